@@ -1,0 +1,142 @@
+/*
+ * rrs.h — C-ABI of the B200-native Rotated Runtime Smooth (RRS) A4W4 linear layer.
+ *
+ * Method: "Rotated Runtime Smooth: Training-Free Activation Smoother for accurate INT4 inference"
+ * (arXiv 2409.20361).  Citations are PAPER.md line numbers (P:n) with section/equation, and the
+ * readings R1..R24 of DESIGN.md §3 where the paper is silent.
+ *
+ * Notation: T tokens (paper's N), K input features, N output features (paper's M),
+ * group size L = 128 (= GEMM K-block), G = K / L groups.
+ *
+ * Conventions shared by every entry point
+ *   - Array arguments are DEVICE pointers (CUDA global memory) allocated and owned by the caller;
+ *     the library never allocates on the hot path and never frees caller memory.  Scratch comes
+ *     from a caller-provided workspace `ws` of at least rrs_workspace_bytes(...) bytes.
+ *   - Row-major, innermost dimension contiguous: X[T][K], W[N][K] (nn.Linear layout), Y[T][ldy].
+ *   - bf16 / f32 data is passed as raw bits (uint16_t for bf16); dtype enums select the format.
+ *   - Packed INT4 (D4): uint8 [rows][K/2]; byte b holds code 2b in bits 0..3 and code 2b+1 in bits
+ *     4..7, two's-complement nibbles; codes lie in [-7, 7] (clamp [-8, 7], R11).
+ *   - GEMM operand layout: int8 [rows][K], one code per byte, columns in the REORDERED order j'
+ *     (sm_100a has no INT4 MMA; the codes go through tcgen05 .kind::i8).
+ *   - Every call enqueues work on `stream` (a cudaStream_t, NULL = legacy default stream) and
+ *     returns without synchronising the host.  Asynchronous device faults surface on a later CUDA call.
+ *   - Validation happens before any launch; on error nothing is enqueued, the status is returned
+ *     and rrs_last_error() (thread-local) describes it.
+ *   - Supported shapes: group == 128; K % 128 == 0 and K in {128,256,...,16384} (2^m) or
+ *     {7168, 14336} (28*2^m, R2); T >= 0; N >= 1.  All pointers 16-byte aligned.
+ *   - X must be bf16 and satisfy the exactness precondition of DESIGN.md R3 (per row, exponent span
+ *     of the nonzero |x| <= 45 - ceil(log2 K)); NaN/Inf inputs are undefined behaviour (not checked).
+ *   - Reentrant; no global state besides the cached device properties and the NCCL communicator
+ *     objects the caller creates.
+ */
+#ifndef RRS_H_
+#define RRS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RRS_OK = 0,
+  RRS_ERR_INVALID_ARGUMENT = 1,  /* null pointer where required, negative size, group != 128 */
+  RRS_ERR_UNSUPPORTED_SHAPE = 2, /* K not 2^m / 28*2^m, K % group != 0 (R7) */
+  RRS_ERR_MISALIGNED = 3,        /* pointer or leading dimension not 16-byte aligned */
+  RRS_ERR_WORKSPACE_TOO_SMALL = 4,
+  RRS_ERR_ARCH = 5,              /* current device is not sm_100 (B200) */
+  RRS_ERR_CUDA = 6,              /* a CUDA runtime/driver call failed (message in rrs_last_error) */
+  RRS_ERR_NCCL = 7               /* an NCCL call failed */
+} rrs_status;
+
+typedef enum { RRS_BF16 = 0, RRS_F32 = 1 } rrs_dtype;
+
+/* rrs_gemm flags */
+#define RRS_GEMM_PLAIN 0x1u /* per-channel A4W4 baseline: one int32 sum over all K, no s_g */
+
+typedef struct rrs_comm_s* rrs_comm_t;
+
+/* Human-readable status name; never NULL. */
+const char* rrs_status_str(int status);
+/* Detail of the last error raised on the calling thread ("" if none). */
+const char* rrs_last_error(void);
+/* ABI version (major * 100 + minor). */
+int rrs_version(void);
+
+/* Workspace bytes needed by rrs_linear / rrs_rotate_smooth_quant for T tokens:
+ * chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xq8[T][K] int8 (+ Y shard and gather
+ * buffers when world > 1), each 256-byte aligned.  Returns 0 for invalid arguments. */
+size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world);
+
+/* Offline reorder helper ("reorder the activations and weights according to the magnitude
+ * of smoothing scales"; R5, R21): perm[j'] = channel of rank j' when channels are sorted by
+ * chan_max descending, ties by ascending channel index.  chan_max: device f32 [K] (>= 0),
+ * typically the rotated calibration activation's chan_max output; perm: device int32 [K]. */
+rrs_status rrs_perm_from_channel_max(const float* chan_max, int64_t K, int32_t* perm, void* stream);
+
+/* Offline weight preparation ("offline rotate the weight matrix", weights
+ * quantised per output channel with symmetric RTN, R12/R13; P:109 step 1 reorders W like X):
+ *   W~ = W . H_K (exact, R1-R3) -> columns permuted by perm (never scaled)
+ *   beta_n = fl(max_j |W~_nj| / 7) (1 if the row is zero, R8); codes rint_even(fl(W~ * fl(7/max))).
+ * W: device bf16 bits [N][K].  perm: device int32 [K] (NULL = identity is NOT accepted: pass it).
+ * Outputs (device, caller-owned; Wq and Wq8 may each be NULL but not both):
+ *   Wq  uint8 [N][K/2] packed INT4;  Wq8 int8 [N][K] GEMM operand;  w_scale f32 [N] = beta_n. */
+rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_t K, int32_t group,
+                               const int32_t* perm, uint8_t* Wq, int8_t* Wq8, float* w_scale,
+                               void* stream);
+
+/* Runtime prologue:
+ *   a1 X~ = X . H_K per token, exact in f64, rounded once to f32 (Eq. 4, R1-R3)
+ *   a2 c_j = max over ALL T tokens of |X~_tj| (Eq. 1, R6)         -> chan_max (optional out)
+ *   a3/a4 s_g = max_{j' in group g} c[perm[j']], 0 -> 1 (P:103(2), R5, R8)  -> s_group
+ *   a5 Z = X~[:, perm] * fl(1/s_g) (Eq. 2, R9)
+ *   a6 alpha_t = fl(max|Z_t| / 7), codes rint_even(fl(Z * fl(7/max))) (R9-R11) -> x_scale, Xq/Xq8
+ * X: device bf16 bits [T][K]; perm: device int32 [K];
+ * outputs: Xq uint8 [T][K/2] (nullable), Xq8 int8 [T][K] (nullable), x_scale f32 [T],
+ *          s_group f32 [K/group], chan_max f32 [K] (nullable: then taken from ws).
+ * ws: device scratch (>= rrs_workspace_bytes(T, 1, K, group, 1) when chan_max == NULL, else may be NULL). */
+rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
+                                   const int32_t* perm, uint8_t* Xq, int8_t* Xq8, float* x_scale,
+                                   float* s_group, float* chan_max, void* ws, size_t ws_bytes,
+                                   void* stream);
+
+/* Fused grouped GEMM (fig:framework (3) P:103, P:109 step 3):
+ *   P_g[t][n] = sum_{j' in g} Xq8[t][j'] * Wq8[n][j']      (int32 in TMEM, exact)
+ *   Y[t][n]   = out_scale * alpha_t * beta_n * sum_g s_g * P_g[t][n]   (f32 scale-accumulate)
+ * out_scale = 1/K after rotation (R1).  flags & RRS_GEMM_PLAIN: per-channel A4W4 baseline
+ * Y = out_scale * alpha_t * beta_n * sum_{all j'} Xq8 Wq8 (s_group ignored, may be NULL).
+ * Xq8 int8 [T][K], x_scale f32 [T], s_group f32 [K/group], Wq8 int8 [N][K], w_scale f32 [N];
+ * Y [T][ldy] in y_dtype (bf16: round-to-nearest-even of the f32 result), ldy >= N, ldy % 8 == 0. */
+rrs_status rrs_gemm(const int8_t* Xq8, const float* x_scale, const float* s_group, const int8_t* Wq8,
+                    const float* w_scale, int64_t T, int64_t N, int64_t K, int32_t group, float out_scale,
+                    uint32_t flags, void* Y, int32_t y_dtype, int64_t ldy, void* stream);
+
+/* Whole layer = rrs_rotate_smooth_quant (into ws) + rrs_gemm with out_scale = 1/K.
+ * comm == NULL: single GPU, Wq8/w_scale hold all N rows.
+ * comm != NULL (column-parallel): Wq8/w_scale hold THIS rank's N/world output rows
+ *   [rank*N/world, (rank+1)*N/world); X is replicated; every rank runs the identical prologue; Y
+ *   receives all N columns through an NCCL all-gather.  N_total % world == 0 required. */
+rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
+                      const int32_t* perm, const int8_t* Wq8, const float* w_scale, int64_t N_total,
+                      void* Y, int32_t y_dtype, int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* Communicator (NCCL over NVLink/NVSwitch).  torch.distributed only ferries the 128-byte id. */
+rrs_status rrs_comm_unique_id(uint8_t id[128]);
+rrs_status rrs_comm_init(rrs_comm_t* comm, int32_t rank, int32_t world, const uint8_t id[128]);
+rrs_status rrs_comm_destroy(rrs_comm_t comm);
+int32_t rrs_comm_world(rrs_comm_t comm);
+int32_t rrs_comm_rank(rrs_comm_t comm);
+
+/* Test-only exports (same kernels, extra stores). */
+/* X~ as f32 [T][K] (natural column order) and chan_max f32 [K] from the a1/a2 kernel. */
+rrs_status rrs_debug_rotate(const void* X, int64_t T, int64_t K, float* Xr, float* chan_max, void* stream);
+/* The tcgen05 GEMM's own int32 group partials P[G][T][N] (read back from TMEM) plus Y. */
+rrs_status rrs_debug_group_partials(const int8_t* Xq8, const int8_t* Wq8, int64_t T, int64_t N, int64_t K,
+                                    int32_t group, int32_t* P, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RRS_H_ */

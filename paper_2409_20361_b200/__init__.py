@@ -1,0 +1,79 @@
+"""B200-native Rotated Runtime Smooth (arXiv 2409.20361) A4W4 linear layer.
+
+Public surface = the C-ABI of include/rrs.h, exposed with the same names by ._lib, plus two thin
+conveniences that only allocate torch device memory and call those entry points:
+
+  RRSLinear      offline weight preparation (rrs_prepare_weights) + forward (rrs_linear)
+  make_comm      NCCL communicator for column-parallel layers; torch.distributed ferries the id
+"""
+from __future__ import annotations
+
+import torch
+
+from ._lib import (EXPORTS, RRSError, lib, rrs_comm_destroy, rrs_comm_init, rrs_comm_unique_id,  # noqa: F401
+                   rrs_debug_group_partials, rrs_debug_rotate, rrs_gemm, rrs_linear, rrs_perm_from_channel_max,
+                   rrs_prepare_weights, rrs_rotate_smooth_quant, rrs_version, rrs_workspace_bytes)
+
+GROUP = 128
+
+
+def shard_rows(N: int, world: int, rank: int) -> tuple[int, int]:
+    """Output-feature range [lo, hi) of `rank` in the column-parallel layout."""
+    if N % world:
+        raise ValueError(f"N={N} not divisible by world={world}")
+    n = N // world
+    return rank * n, (rank + 1) * n
+
+
+def calibrate_perm(X_cal: torch.Tensor, stream=None) -> torch.Tensor:
+    """Offline reorder (R5): rotate the calibration activation, take its channel max, sort (GPU)."""
+    T, K = X_cal.shape
+    dev = X_cal.device
+    Xr = torch.empty((T, K), dtype=torch.float32, device=dev)
+    cm = torch.empty(K, dtype=torch.float32, device=dev)
+    rrs_debug_rotate(X_cal, Xr, cm, stream=stream)
+    perm = torch.empty(K, dtype=torch.int32, device=dev)
+    rrs_perm_from_channel_max(cm, perm, stream=stream)
+    return perm
+
+
+class RRSLinear:
+    """Y = RRS-A4W4(X) @ W^T for a bf16 nn.Linear weight W[N][K] (column shard when comm is given)."""
+
+    def __init__(self, W: torch.Tensor, perm: torch.Tensor, comm=None, world: int = 1, rank: int = 0,
+                 keep_packed: bool = False, stream=None):
+        N, K = W.shape
+        self.K, self.N_total = K, N
+        self.comm, self.world, self.rank = comm, world, rank
+        lo, hi = shard_rows(N, world, rank)
+        Wl = W[lo:hi].contiguous()
+        dev = W.device
+        self.perm = perm.to(device=dev, dtype=torch.int32).contiguous()
+        self.Wq8 = torch.empty((hi - lo, K), dtype=torch.int8, device=dev)
+        self.Wq = torch.empty((hi - lo, K // 2), dtype=torch.uint8, device=dev) if keep_packed else None
+        self.w_scale = torch.empty(hi - lo, dtype=torch.float32, device=dev)
+        rrs_prepare_weights(Wl, self.perm, self.Wq, self.Wq8, self.w_scale, stream=stream)
+        self._ws = None
+
+    def workspace(self, T: int, device) -> torch.Tensor:
+        need = rrs_workspace_bytes(T, self.N_total, self.K, GROUP, self.world)
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+        return self._ws
+
+    def __call__(self, X: torch.Tensor, out_dtype=torch.bfloat16, Y: torch.Tensor | None = None, stream=None):
+        T = X.shape[0]
+        if Y is None:
+            Y = torch.empty((T, self.N_total), dtype=out_dtype, device=X.device)
+        rrs_linear(X, self.perm, self.Wq8, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
+                   comm=self.comm, stream=stream)
+        return Y
+
+
+def make_comm(group=None):
+    """NCCL communicator over the ranks of a torch.distributed group (rank 0's id is broadcast)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = [rrs_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0, group=group)
+    return rrs_comm_init(rank, world, uid[0]), rank, world

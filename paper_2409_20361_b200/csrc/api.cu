@@ -1,0 +1,343 @@
+// C-ABI host layer of librrs (include/rrs.h): validation, workspace carving, launches, NCCL comm.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "../../include/rrs.h"
+#include "kernels.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+rrs_status fail(rrs_status s, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+rrs_status fail(rrs_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+rrs_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(RRS_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+struct DevInfo {
+  int major = 0, minor = 0, nsm = 0;
+};
+
+// per-device cached properties
+DevInfo device_info(int& dev, cudaError_t& err) {
+  static std::mutex mu;
+  static DevInfo cache[64];
+  static bool have[64] = {};
+  err = cudaGetDevice(&dev);
+  if (err != cudaSuccess || dev < 0 || dev >= 64) return DevInfo{};
+  std::lock_guard<std::mutex> lk(mu);
+  if (!have[dev]) {
+    cudaDeviceProp p;
+    err = cudaGetDeviceProperties(&p, dev);
+    if (err != cudaSuccess) return DevInfo{};
+    cache[dev].major = p.major;
+    cache[dev].minor = p.minor;
+    cache[dev].nsm = p.multiProcessorCount;
+    have[dev] = true;
+  }
+  return cache[dev];
+}
+
+rrs_status check_arch(int& nsm) {
+  int dev;
+  cudaError_t e;
+  DevInfo d = device_info(dev, e);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDeviceProperties");
+  if (d.major != 10 || d.minor != 0)
+    return fail(RRS_ERR_ARCH, "device %d is sm_%d%d; librrs is built for sm_100a (B200) only", dev, d.major,
+                d.minor);
+  nsm = d.nsm;
+  return RRS_OK;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+rrs_status check_shape(int64_t T, int64_t K, int32_t group) {
+  if (T < 0) return fail(RRS_ERR_INVALID_ARGUMENT, "T=%lld < 0", (long long)T);
+  if (group != 128) return fail(RRS_ERR_INVALID_ARGUMENT, "group=%d: only 128 is supported (P:189)", group);
+  if (K <= 0 || K % group) return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld not a positive multiple of group %d", (long long)K, group);
+  if (!rrs::prologue_supports_k(K))
+    return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld: need 2^m in [128,16384] or 28*2^m in {7168,14336}", (long long)K);
+  return RRS_OK;
+}
+
+struct Workspace {
+  float* chan_max;
+  float* s_group;
+  float* x_scale;
+  int8_t* Xq8;
+  void* y_shard;
+  void* y_gather;
+};
+
+size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t world, Workspace* w) {
+  size_t off = 0;
+  auto take = [&](size_t bytes) -> void* {
+    void* p = base ? static_cast<char*>(base) + off : nullptr;
+    off += align256(bytes);
+    return p;
+  };
+  Workspace tmp;
+  Workspace& ws = w ? *w : tmp;
+  ws.chan_max = static_cast<float*>(take(sizeof(float) * K));
+  ws.s_group = static_cast<float*>(take(sizeof(float) * (K / group)));
+  ws.x_scale = static_cast<float*>(take(sizeof(float) * (T > 0 ? T : 1)));
+  ws.Xq8 = static_cast<int8_t*>(take((size_t)T * K));
+  ws.y_shard = nullptr;
+  ws.y_gather = nullptr;
+  if (world > 1) {
+    const int64_t ns = N / world;
+    ws.y_shard = take((size_t)T * ns * 4);
+    ws.y_gather = take((size_t)T * N * 4);
+  }
+  return off;
+}
+
+}  // namespace
+
+struct rrs_comm_s {
+  ncclComm_t nccl;
+  int rank, world;
+};
+
+extern "C" {
+
+const char* rrs_status_str(int s) {
+  switch (s) {
+    case RRS_OK: return "RRS_OK";
+    case RRS_ERR_INVALID_ARGUMENT: return "RRS_ERR_INVALID_ARGUMENT";
+    case RRS_ERR_UNSUPPORTED_SHAPE: return "RRS_ERR_UNSUPPORTED_SHAPE";
+    case RRS_ERR_MISALIGNED: return "RRS_ERR_MISALIGNED";
+    case RRS_ERR_WORKSPACE_TOO_SMALL: return "RRS_ERR_WORKSPACE_TOO_SMALL";
+    case RRS_ERR_ARCH: return "RRS_ERR_ARCH";
+    case RRS_ERR_CUDA: return "RRS_ERR_CUDA";
+    case RRS_ERR_NCCL: return "RRS_ERR_NCCL";
+    default: return "RRS_ERR_UNKNOWN";
+  }
+}
+
+const char* rrs_last_error(void) { return g_last_error.c_str(); }
+
+int rrs_version(void) { return 100; }
+
+size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world) {
+  if (T < 0 || K <= 0 || group <= 0 || K % group || world < 1 || (world > 1 && (N <= 0 || N % world))) return 0;
+  return carve(nullptr, T, N, K, group, world, nullptr);
+}
+
+rrs_status rrs_perm_from_channel_max(const float* chan_max, int64_t K, int32_t* perm, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (!chan_max || !perm) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (K <= 0 || K > 16384) return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld out of range", (long long)K);
+  cudaError_t e = rrs::launch_perm_rank(chan_max, K, perm, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "perm_rank_kernel");
+}
+
+rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_t K, int32_t group,
+                               const int32_t* perm, uint8_t* Wq, int8_t* Wq8, float* w_scale, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (w_dtype != RRS_BF16) return fail(RRS_ERR_INVALID_ARGUMENT, "W must be bf16 (R17)");
+  if (N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "N=%lld < 1", (long long)N);
+  if (rrs_status s = check_shape(N, K, group)) return s;
+  if (!W || !perm || !w_scale || (!Wq && !Wq8)) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(W) || !aligned16(perm) || !aligned16(Wq) || !aligned16(Wq8))
+    return fail(RRS_ERR_MISALIGNED, "pointers must be 16-byte aligned");
+  cudaError_t e = rrs::launch_fwht_quant(static_cast<const uint16_t*>(W), N, K, perm, nullptr, nullptr, Wq, Wq8,
+                                         w_scale, nsm, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "fwht_quant_kernel (weights)");
+}
+
+static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* perm, uint8_t* Xq, int8_t* Xq8,
+                           float* x_scale, float* s_group, float* chan_max, int nsm, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * K, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
+  e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), nullptr,
+                              nsm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fwht_colmax_kernel");
+  e = rrs::launch_fwht_quant(static_cast<const uint16_t*>(X), T, K, perm, reinterpret_cast<const unsigned*>(chan_max),
+                             s_group, Xq, Xq8, x_scale, nsm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fwht_quant_kernel");
+  return RRS_OK;
+}
+
+rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
+                                   const int32_t* perm, uint8_t* Xq, int8_t* Xq8, float* x_scale, float* s_group,
+                                   float* chan_max, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (x_dtype != RRS_BF16) return fail(RRS_ERR_INVALID_ARGUMENT, "X must be bf16 (R17)");
+  if (rrs_status s = check_shape(T, K, group)) return s;
+  if ((T > 0 && !X) || !perm || !s_group || (T > 0 && !x_scale))
+    return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!aligned16(X) || !aligned16(perm) || !aligned16(Xq) || !aligned16(Xq8))
+    return fail(RRS_ERR_MISALIGNED, "pointers must be 16-byte aligned");
+  if (!chan_max) {
+    Workspace w;
+    const size_t need = carve(ws, T, 1, K, group, 1, &w);
+    if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
+    chan_max = w.chan_max;
+  }
+  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, nsm, static_cast<cudaStream_t>(stream));
+}
+
+static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int8_t* Wq8, const float* w_scale,
+                              int64_t T, int64_t N, int64_t K, int32_t group, const void* Y, int64_t ldy) {
+  if (T < 0 || N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "T=%lld N=%lld", (long long)T, (long long)N);
+  if (group != 128) return fail(RRS_ERR_INVALID_ARGUMENT, "group=%d: only 128 supported", group);
+  if (K <= 0 || K % group) return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld", (long long)K);
+  if (T > 0 && (!Xq8 || !x_scale || !Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (!Wq8 || !w_scale) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (ldy < N) return fail(RRS_ERR_INVALID_ARGUMENT, "ldy=%lld < N=%lld", (long long)ldy, (long long)N);
+  if (!aligned16(Xq8) || !aligned16(Wq8) || !aligned16(Y) || ldy % 8)
+    return fail(RRS_ERR_MISALIGNED, "pointers 16-byte aligned and ldy %% 8 == 0 required");
+  return RRS_OK;
+}
+
+rrs_status rrs_gemm(const int8_t* Xq8, const float* x_scale, const float* s_group, const int8_t* Wq8,
+                    const float* w_scale, int64_t T, int64_t N, int64_t K, int32_t group, float out_scale,
+                    uint32_t flags, void* Y, int32_t y_dtype, int64_t ldy, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (rrs_status s = gemm_checks(Xq8, x_scale, Wq8, w_scale, T, N, K, group, Y, ldy)) return s;
+  const bool plain = (flags & RRS_GEMM_PLAIN) != 0;
+  if (!plain && !s_group) return fail(RRS_ERR_INVALID_ARGUMENT, "s_group is NULL");
+  if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
+  if (T == 0) return RRS_OK;
+  rrs::GemmArgs a{Xq8, x_scale, s_group, Wq8, w_scale, T, N, K, group, out_scale, plain, Y, y_dtype, ldy, nullptr};
+  cudaError_t e = rrs::launch_gemm(a, nsm, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
+}
+
+rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group, const int32_t* perm,
+                      const int8_t* Wq8, const float* w_scale, int64_t N_total, void* Y, int32_t y_dtype,
+                      int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (x_dtype != RRS_BF16) return fail(RRS_ERR_INVALID_ARGUMENT, "X must be bf16 (R17)");
+  if (rrs_status s = check_shape(T, K, group)) return s;
+  const int world = comm ? comm->world : 1;
+  if (N_total < 1 || N_total % world)
+    return fail(RRS_ERR_INVALID_ARGUMENT, "N_total=%lld must be a positive multiple of world=%d", (long long)N_total, world);
+  const int64_t n_local = N_total / world;
+  if ((T > 0 && !X) || !perm) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
+  Workspace w;
+  const size_t need = carve(ws, T, N_total, K, group, world, &w);
+  if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
+  if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, nsm, st)) return s;
+  if (T == 0) return RRS_OK;
+  const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
+  const int esz = y_dtype == RRS_F32 ? 4 : 2;
+  if (world == 1) {
+    if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy)) return s;
+    rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N_total, K, group, out_scale, false, Y, y_dtype, ldy, nullptr};
+    cudaError_t e = rrs::launch_gemm(a, nsm, st);
+    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
+  }
+  // column-parallel: local shard [T][n_local] -> all-gather [world][T][n_local] -> Y[T][ldy]
+  if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, n_local, K, group, w.y_shard, n_local)) return s;
+  if (ldy < N_total || !aligned16(Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "Y / ldy");
+  rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, n_local, K, group, out_scale, false, w.y_shard, y_dtype, n_local, nullptr};
+  cudaError_t e = rrs::launch_gemm(a, nsm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "rrs_gemm kernel");
+  ncclResult_t r = ncclAllGather(w.y_shard, w.y_gather, (size_t)T * n_local * esz, ncclUint8, comm->nccl, st);
+  if (r != ncclSuccess) return fail(RRS_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+  e = rrs::launch_relayout_shards(w.y_gather, Y, T, n_local, world, ldy, esz, st);
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "relayout kernel");
+}
+
+rrs_status rrs_comm_unique_id(uint8_t id[128]) {
+  g_last_error.clear();
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId u;
+  ncclResult_t r = ncclGetUniqueId(&u);
+  if (r != ncclSuccess) return fail(RRS_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(r));
+  memcpy(id, &u, 128);
+  return RRS_OK;
+}
+
+rrs_status rrs_comm_init(rrs_comm_t* comm, int32_t rank, int32_t world, const uint8_t id[128]) {
+  g_last_error.clear();
+  if (!comm || !id || world < 1 || rank < 0 || rank >= world) return fail(RRS_ERR_INVALID_ARGUMENT, "comm args");
+  ncclUniqueId u;
+  memcpy(&u, id, 128);
+  auto* c = new rrs_comm_s{};
+  ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    return fail(RRS_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+  }
+  c->rank = rank;
+  c->world = world;
+  *comm = c;
+  return RRS_OK;
+}
+
+rrs_status rrs_comm_destroy(rrs_comm_t comm) {
+  g_last_error.clear();
+  if (!comm) return RRS_OK;
+  ncclResult_t r = ncclCommDestroy(comm->nccl);
+  delete comm;
+  return r == ncclSuccess ? RRS_OK : fail(RRS_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
+}
+
+int32_t rrs_comm_world(rrs_comm_t comm) { return comm ? comm->world : 1; }
+int32_t rrs_comm_rank(rrs_comm_t comm) { return comm ? comm->rank : 0; }
+
+rrs_status rrs_debug_rotate(const void* X, int64_t T, int64_t K, float* Xr, float* chan_max, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (rrs_status s = check_shape(T, K, 128)) return s;
+  if (!chan_max || (T > 0 && (!X || !Xr))) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * K, st);
+  if (e != cudaSuccess) return cuda_fail(e, "memset");
+  e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr, nsm, st);
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "fwht_colmax_kernel");
+}
+
+rrs_status rrs_debug_group_partials(const int8_t* Xq8, const int8_t* Wq8, int64_t T, int64_t N, int64_t K,
+                                    int32_t group, int32_t* P, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (!P) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  // the GEMM needs valid scale pointers; partials do not depend on them: use a scratch Y in P's tail? No:
+  // the debug launch passes P and a null Y; the kernel skips the Y store when Y == nullptr.
+  if (T < 0 || N < 1 || group != 128 || K <= 0 || K % group) return fail(RRS_ERR_INVALID_ARGUMENT, "shape");
+  if (!aligned16(Xq8) || !aligned16(Wq8)) return fail(RRS_ERR_MISALIGNED, "alignment");
+  if (T == 0) return RRS_OK;
+  rrs::GemmArgs a{Xq8, nullptr, nullptr, Wq8, nullptr, T, N, K, group, 1.0f, false, nullptr, RRS_F32, N, P};
+  cudaError_t e = rrs::launch_gemm(a, nsm, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel (debug partials)");
+}
+
+}  // extern "C"

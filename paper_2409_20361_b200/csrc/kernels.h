@@ -1,0 +1,36 @@
+// Internal host-side launch entry points of the RRS kernels (not part of the public C-ABI).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rrs {
+
+bool prologue_supports_k(int64_t K);
+cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
+                               int nsm, cudaStream_t st);
+cudaError_t launch_fwht_quant(const uint16_t* X, int64_t T, int64_t K, const int32_t* perm,
+                              const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
+                              float* scale, int nsm, cudaStream_t st);
+cudaError_t launch_perm_rank(const float* c, int64_t K, int32_t* perm, cudaStream_t st);
+
+struct GemmArgs {
+  const int8_t* Xq8;      // [T][K] int8 codes (reordered order)
+  const float* x_scale;   // [T]
+  const float* s_group;   // [G]
+  const int8_t* Wq8;      // [N][K]
+  const float* w_scale;   // [N]
+  int64_t T, N, K;
+  int group;
+  float out_scale;
+  bool plain;             // per-channel A4W4 baseline: one int32 accumulation over all K, no s_g
+  void* Y;                // [T][ldy]
+  int y_dtype;            // 0 = bf16, 1 = f32
+  int64_t ldy;
+  int32_t* P_debug;       // optional [G][T][N] export of the int32 group partials (test only)
+};
+cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st);
+
+cudaError_t launch_relayout_shards(const void* src, void* dst, int64_t T, int64_t n_shard, int world,
+                                   int64_t ldy, int elem_bytes, cudaStream_t st);
+
+}  // namespace rrs

@@ -1,0 +1,311 @@
+"""CUDA path vs the CPU oracle, element by element, through the C-ABI (paper_2409_20361_b200._lib).
+
+Bar (BASELINE.json north_star): bit-exact on X~, chan_max, s_group, alpha_t, every code,
+every packed byte, beta_n, Wq and every int32 group partial P_g; Y f32 within normalised error 1e-5;
+Y bf16 within 1 bf16 ulp.  Sizes span several 128x256 GEMM tiles and ragged T / N tails.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2409_20361_b200 as rrs  # noqa: E402
+from oracle import rrs_oracle as o  # noqa: E402
+from rrs_synth import WORKLOADS, bf16_bits_to_f64, make_activations, make_layer, make_weights  # noqa: E402
+
+from _parity import bf16_ulp_error, dev_bf16, oracle_layer, y_normalised_error  # noqa: E402
+
+DEV = "cuda"
+
+
+def _perm(Xc_bits):
+    return o.calibrate_perm(bf16_bits_to_f64(Xc_bits)).astype(np.int32)
+
+
+def _u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _run_prologue(X_bits, perm):
+    T, K = X_bits.shape
+    X = dev_bf16(X_bits)
+    p = torch.from_numpy(perm).to(DEV)
+    Xq = torch.empty((T, K // 2), dtype=torch.uint8, device=DEV)
+    Xq8 = torch.empty((T, K), dtype=torch.int8, device=DEV)
+    xs = torch.empty(T, dtype=torch.float32, device=DEV)
+    sg = torch.empty(K // 128, dtype=torch.float32, device=DEV)
+    cm = torch.empty(K, dtype=torch.float32, device=DEV)
+    rrs.rrs_rotate_smooth_quant(X, p, Xq, Xq8, xs, sg, chan_max=cm)
+    torch.cuda.synchronize()
+    return dict(Xq=Xq.cpu().numpy(), Xq8=Xq8.cpu().numpy(), alpha=xs.cpu().numpy(), s_group=sg.cpu().numpy(),
+                chan_max=cm.cpu().numpy())
+
+
+def _run_weights(W_bits, perm):
+    N, K = W_bits.shape
+    Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=DEV)
+    Wq8 = torch.empty((N, K), dtype=torch.int8, device=DEV)
+    ws = torch.empty(N, dtype=torch.float32, device=DEV)
+    rrs.rrs_prepare_weights(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), Wq, Wq8, ws)
+    torch.cuda.synchronize()
+    return Wq.cpu().numpy(), Wq8, ws
+
+
+# ------------------------------------------------------------------------------------- a1 / a2
+
+@pytest.mark.parametrize("K,T,profile", [(128, 5, "channel"), (256, 37, "tiny"), (1024, 64, "spike"),
+                                         (4096, 33, "channel"), (8192, 9, "mixed"), (16384, 3, "channel"),
+                                         (7168, 11, "spike"), (14336, 13, "spike")])
+def test_rotation_and_channel_max_bitexact(K, T, profile):
+    X_bits = make_activations(profile, T, K, 101, 202)
+    Xr = torch.empty((T, K), dtype=torch.float32, device=DEV)
+    cm = torch.empty(K, dtype=torch.float32, device=DEV)
+    rrs.rrs_debug_rotate(dev_bf16(X_bits), Xr, cm)
+    torch.cuda.synchronize()
+    ref = o.rotate(bf16_bits_to_f64(X_bits))
+    assert np.array_equal(_u32(Xr), ref.view(np.uint32))
+    assert np.array_equal(_u32(cm), o.channel_max(ref).view(np.uint32))
+
+
+# ------------------------------------------------------------------------------------- a3-a6
+
+@pytest.mark.parametrize("K,T,profile", [(256, 8, "tiny"), (256, 300, "channel"), (4096, 129, "channel"),
+                                         (14336, 40, "spike"), (8192, 64, "mixed"), (512, 1, "channel")])
+def test_prologue_bitexact(K, T, profile):
+    X_bits = make_activations(profile, T, K, 303, 404)
+    perm = _perm(make_activations(profile, 64, K, 303, 405))
+    g = _run_prologue(X_bits, perm)
+    Xr = o.rotate(bf16_bits_to_f64(X_bits))
+    c = o.channel_max(Xr)
+    s = o.group_scales(c, perm, 128)
+    q, a = o.smooth_quant(Xr, perm, s, 128)
+    assert np.array_equal(g["chan_max"].view(np.uint32), c.view(np.uint32))
+    assert np.array_equal(g["s_group"].view(np.uint32), s.view(np.uint32))
+    assert np.array_equal(g["alpha"].view(np.uint32), a.view(np.uint32))
+    assert np.array_equal(g["Xq8"], q)
+    assert np.array_equal(g["Xq"], o.pack_int4(q))
+
+
+def test_prologue_zero_rows_and_identity_perm():
+    """R8: all-zero tokens -> alpha 1, codes 0; zero channels make no group scale 0 unless the group is."""
+    K, T = 512, 20
+    X_bits = make_activations("channel", T, K, 1, 2)
+    X_bits[[0, 7, 19]] = 0
+    perm = np.arange(K, dtype=np.int32)
+    g = _run_prologue(X_bits, perm)
+    r = o.rrs_linear(bf16_bits_to_f64(X_bits), np.zeros((1, K)), perm, keep_partials=False)
+    assert np.array_equal(g["alpha"].view(np.uint32), r["alpha"].view(np.uint32))
+    assert np.all(g["alpha"][[0, 7, 19]] == 1.0) and not g["Xq8"][[0, 7, 19]].any()
+    assert np.array_equal(g["Xq8"], r["q"])
+
+
+def test_prologue_all_zero_activation():
+    K, T = 256, 4
+    g = _run_prologue(np.zeros((T, K), np.uint16), np.arange(K, dtype=np.int32))
+    assert np.all(g["s_group"] == 1.0) and np.all(g["alpha"] == 1.0) and not g["Xq8"].any()
+
+
+# ------------------------------------------------------------------------------------- a7
+
+@pytest.mark.parametrize("K,N", [(256, 256), (4096, 300), (14336, 64)])
+def test_prepare_weights_bitexact(K, N):
+    W_bits = make_weights(N, K, 77)
+    perm = _perm(make_activations("channel", 64, K, 5, 6))
+    Wq, Wq8, ws = _run_weights(W_bits, perm)
+    qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits), perm)
+    assert np.array_equal(Wq8.cpu().numpy(), qw)
+    assert np.array_equal(Wq, o.pack_int4(qw))
+    assert np.array_equal(_u32(ws), beta.view(np.uint32))
+
+
+# ------------------------------------------------------------------------------------- a8 / a9
+
+@pytest.mark.parametrize("T,N,K", [(8, 256, 256), (300, 600, 512), (129, 257, 4096), (1, 16, 128), (256, 512, 1024)])
+def test_group_partials_bitexact(T, N, K):
+    rng = np.random.default_rng(T * 7 + N)
+    q = rng.integers(-7, 8, size=(T, K)).astype(np.int8)
+    qw = rng.integers(-7, 8, size=(N, K)).astype(np.int8)
+    q[0, :] = 7   # extreme partials: +-49 * 128
+    qw[0, :] = -7
+    P = torch.empty((K // 128, T, N), dtype=torch.int32, device=DEV)
+    rrs.rrs_debug_group_partials(torch.from_numpy(q).to(DEV), torch.from_numpy(qw).to(DEV), P)
+    torch.cuda.synchronize()
+    assert np.array_equal(P.cpu().numpy(), o.group_partials(q, qw, 128))
+
+
+def _gemm_case(T, N, K, profile="channel", seed=0):
+    X_bits = make_activations(profile, T, K, 900 + seed, 901 + seed)
+    W_bits = make_weights(N, K, 902 + seed)
+    perm = _perm(make_activations(profile, 64, K, 900 + seed, 903 + seed))
+    ref = oracle_layer(X_bits, W_bits, perm)
+    return X_bits, W_bits, perm, ref
+
+
+@pytest.mark.parametrize("T,N,K,profile", [(8, 256, 256, "tiny"), (300, 600, 512, "channel"),
+                                           (129, 520, 4096, "channel"), (200, 264, 14336, "spike"),
+                                           (64, 512, 8192, "mixed")])
+def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile):
+    X_bits, W_bits, perm, ref = _gemm_case(T, N, K, profile)
+    Xq8 = torch.from_numpy(ref["q"]).to(DEV)
+    Wq8 = torch.from_numpy(ref["qw"]).to(DEV)
+    xs = torch.from_numpy(ref["alpha"]).to(DEV)
+    sg = torch.from_numpy(ref["s_group"]).to(DEV)
+    ws = torch.from_numpy(ref["beta"]).to(DEV)
+    ldy = (N + 7) // 8 * 8
+    Yf = torch.full((T, ldy), float("nan"), dtype=torch.float32, device=DEV)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf[:, :N], 1.0 / K)
+    Yb = torch.zeros((T, ldy), dtype=torch.bfloat16, device=DEV)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yb[:, :N], 1.0 / K)
+    torch.cuda.synchronize()
+    Yf_np = Yf.cpu().numpy()
+    assert np.isnan(Yf_np[:, N:]).all()  # nothing written past N
+    assert y_normalised_error(Yf_np[:, :N], ref) <= 1e-5
+    assert bf16_ulp_error(Yb[:, :N].float().cpu().numpy(), ref["Y"]) <= 1.0
+
+
+def test_plain_gemm_matches_per_channel_baseline():
+    """RRS_GEMM_PLAIN: Y = alpha beta sum_all q qw / K (per-channel A4W4)."""
+    X_bits, W_bits, perm, ref = _gemm_case(130, 300, 1024)
+    Xq8 = torch.from_numpy(ref["q"]).to(DEV)
+    Wq8 = torch.from_numpy(ref["qw"]).to(DEV)
+    Y = torch.empty((130, 304), dtype=torch.float32, device=DEV)
+    rrs.rrs_gemm(Xq8, torch.from_numpy(ref["alpha"]).to(DEV), None, Wq8, torch.from_numpy(ref["beta"]).to(DEV),
+                 Y[:, :300], 1.0 / 1024, plain=True)
+    torch.cuda.synchronize()
+    Pall = ref["P"].astype(np.int64).sum(axis=0).astype(np.float64)
+    exp = Pall * ref["alpha"].astype(np.float64)[:, None] * ref["beta"].astype(np.float64)[None, :] / 1024
+    den = np.abs(ref["P"]).astype(np.float64).sum(0) * ref["alpha"][:, None] * ref["beta"][None, :] / 1024
+    err = np.abs(Y[:, :300].cpu().numpy() - exp)
+    assert np.all(err <= 1e-5 * np.maximum(den, 1e-30))
+
+
+# ------------------------------------------------------------------------------------- whole layer
+
+@pytest.mark.parametrize("wl,T,N", [("c1_tiny", None, None), ("c2_llama2_7b_qo", 257, 520),
+                                    ("c3_llama3_8b_down", 130, 264)])
+def test_rrs_linear_end_to_end(wl, T, N):
+    w = WORKLOADS[wl]
+    X_bits, W_bits, Xc = make_layer(w, T=T, N=N, T_cal=64)
+    T, N = X_bits.shape[0], W_bits.shape[0]
+    perm = _perm(Xc)
+    ref = oracle_layer(X_bits, W_bits, perm)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), keep_packed=True)
+    Y = layer(dev_bf16(X_bits), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert np.array_equal(layer.Wq.cpu().numpy(), ref["Wq"])
+    assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
+    Yb = layer(dev_bf16(X_bits), out_dtype=torch.bfloat16)
+    assert bf16_ulp_error(Yb.float().cpu().numpy(), ref["Y"]) <= 1.0
+
+
+def test_rrs_linear_equals_prologue_plus_gemm_bitwise():
+    X_bits, W_bits, perm, ref = _gemm_case(200, 512, 4096)
+    X = dev_bf16(X_bits)
+    p = torch.from_numpy(perm).to(DEV)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), p)
+    Y1 = layer(X, out_dtype=torch.float32)
+    Xq8 = torch.empty((200, 4096), dtype=torch.int8, device=DEV)
+    xs = torch.empty(200, dtype=torch.float32, device=DEV)
+    sg = torch.empty(32, dtype=torch.float32, device=DEV)
+    ws = torch.empty(rrs.rrs_workspace_bytes(200, 512, 4096), dtype=torch.uint8, device=DEV)
+    rrs.rrs_rotate_smooth_quant(X, p, None, Xq8, xs, sg, ws=ws)
+    Y2 = torch.empty_like(Y1)
+    rrs.rrs_gemm(Xq8, xs, sg, layer.Wq8, layer.w_scale, Y2, 1.0 / 4096)
+    torch.cuda.synchronize()
+    assert torch.equal(Y1, Y2)
+    assert y_normalised_error(Y1.cpu().numpy(), ref) <= 1e-5
+
+
+def test_deterministic_run_to_run():
+    X_bits, W_bits, perm, _ = _gemm_case(300, 600, 1024)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV))
+    X = dev_bf16(X_bits)
+    a = layer(X, out_dtype=torch.float32)
+    b = layer(X, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+
+
+def test_comm_world1_path_equals_single_gpu():
+    """Column-parallel path with a 1-rank NCCL communicator (shard -> all-gather -> relayout)."""
+    X_bits, W_bits, perm, ref = _gemm_case(130, 512, 1024)
+    uid = rrs.rrs_comm_unique_id()
+    comm = rrs.rrs_comm_init(0, 1, uid)
+    try:
+        p = torch.from_numpy(perm).to(DEV)
+        single = rrs.RRSLinear(dev_bf16(W_bits), p)
+        par = rrs.RRSLinear(dev_bf16(W_bits), p, comm=comm, world=1, rank=0)
+        X = dev_bf16(X_bits)
+        a = single(X, out_dtype=torch.float32)
+        b = par(X, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert torch.equal(a, b)
+    finally:
+        rrs.rrs_comm_destroy(comm)
+
+
+def test_perm_helper_matches_oracle():
+    K = 4096
+    Xc = make_activations("channel", 64, K, 11, 12)
+    Xr = torch.empty((64, K), dtype=torch.float32, device=DEV)
+    cm = torch.empty(K, dtype=torch.float32, device=DEV)
+    rrs.rrs_debug_rotate(dev_bf16(Xc), Xr, cm)
+    perm = torch.empty(K, dtype=torch.int32, device=DEV)
+    rrs.rrs_perm_from_channel_max(cm, perm)
+    torch.cuda.synchronize()
+    assert np.array_equal(perm.cpu().numpy(), _perm(Xc))
+    # ties: ascending index (R21)
+    c = torch.tensor([5, 5, 7, 5, 0, 7] + [0] * 122, dtype=torch.float32, device=DEV)
+    pp = torch.empty(128, dtype=torch.int32, device=DEV)
+    rrs.rrs_perm_from_channel_max(c, pp)
+    assert np.array_equal(pp.cpu().numpy(), o.perm_from_channel_max(c.cpu().numpy()))
+
+
+def test_invalid_arguments_raise():
+    X = torch.zeros((4, 256), dtype=torch.bfloat16, device=DEV)
+    p = torch.arange(256, dtype=torch.int32, device=DEV)
+    xs = torch.empty(4, device=DEV)
+    sg = torch.empty(2, device=DEV)
+    with pytest.raises(rrs.RRSError) as e:
+        rrs.rrs_rotate_smooth_quant(X, p, None, None, xs, sg, chan_max=torch.empty(256, device=DEV), group=64)
+    assert e.value.status == 1
+    Xbad = torch.zeros((4, 96 * 3), dtype=torch.bfloat16, device=DEV)
+    with pytest.raises(rrs.RRSError) as e:
+        rrs.rrs_rotate_smooth_quant(Xbad, p, None, None, xs, sg, chan_max=torch.empty(288, device=DEV))
+    assert e.value.status == 2
+
+
+# ------------------------------------------------------------------------------------- full size, sampled
+
+def test_full_size_c2_sampled_rows():
+    """BASELINE configs[1] at full size (2048 x 4096 x 4096), same launch configuration as bench.py.
+
+    The prologue is checked in full (oracle rotation of all 2048 tokens); Y on 64 sampled token rows
+    (the oracle's grouped GEMM restricted to those rows, exact same arithmetic)."""
+    w = WORKLOADS["c2_llama2_7b_qo"]
+    X_bits, W_bits, Xc = make_layer(w, index=1)
+    perm = _perm(Xc[:256])
+    X = dev_bf16(X_bits)
+    p = torch.from_numpy(perm).to(DEV)
+    g = _run_prologue(X_bits, perm)
+    Xr = o.rotate(bf16_bits_to_f64(X_bits))
+    c = o.channel_max(Xr)
+    s = o.group_scales(c, perm, 128)
+    q, a = o.smooth_quant(Xr, perm, s, 128)
+    assert np.array_equal(g["s_group"].view(np.uint32), s.view(np.uint32))
+    assert np.array_equal(g["alpha"].view(np.uint32), a.view(np.uint32))
+    assert np.array_equal(g["Xq"], o.pack_int4(q))
+    layer = rrs.RRSLinear(dev_bf16(W_bits), p)
+    Y = layer(X, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    rows = np.random.default_rng(0).choice(w.T, size=64, replace=False)
+    qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits), perm)
+    assert np.array_equal(layer.w_scale.cpu().numpy().view(np.uint32), beta.view(np.uint32))
+    P = o.group_partials(q[rows], qw, 128)
+    Yref = o.scale_accumulate(P, s, a[rows], beta, 1.0 / w.K)
+    ref = dict(P=P, s_group=s, alpha=a[rows], beta=beta, out_scale=1.0 / w.K, Y=Yref)
+    assert y_normalised_error(Y.cpu().numpy()[rows], ref) <= 1e-5
