@@ -1,0 +1,383 @@
+#!/usr/bin/env python
+"""bench.py — RRS A4W4 linear layer on B200 (one JSON line on rank 0).
+
+    python bench.py [--gpus N --steps K --warmup W] [--workload c2_llama2_7b_qo] [--out-dtype bf16]
+    python bench.py --impl reference ...      # the CPU oracle as the reference arm (rank 0 only)
+    torchrun --nproc-per-node N bench.py --gpus N ...   # column-parallel W over N GPUs + NCCL all-gather
+
+A step is one pass of the whole hot path (a7 is the offline weight
+preparation, timed once and reported separately) over one batch of synthetic input already resident in HBM:
+    rrs_rotate_smooth_quant -> rrs_gemm (-> rrs_allgather_columns when N > 1).
+L2 is flushed (256 MiB write) before every timed step; each step is timed with CUDA events on the launching
+stream and the bracketing barrier + synchronize surround the whole timed loop.  Multi-GPU times are the max
+over ranks.  Inputs: seeded synthetic LLaMA-like activations and N(0, 0.02^2) weights (rrs_synth).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from rrs_synth import WORKLOADS, make_layer  # noqa: E402
+
+METRIC = "RRS A4W4 linear TOPS"
+INT8_OVER_BF16 = 2.0  # nominal dense int8 : bf16 tensor ratio (4.5 : 2.25 PFLOP/s, B200_PROFILING.md)
+
+
+def peaks():
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
+    f = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(f):
+        with open(f) as fh:
+            m = json.load(fh)
+        p = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]),
+             "bf16_tflops_sustained": float(m.get("bf16_tflops_sustained", m["bf16_tflops"])),
+             "src": "measured (MEASURED_PEAKS.json)"}
+    return p
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------ GPU arm
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_20361_b200 as rrs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    w = WORKLOADS[args.workload]
+    T, K, N = w.T, w.K, w.N
+    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
+    esz = 2 if args.out_dtype == "bf16" else 4
+
+    # ---- inputs (seeded, synthetic), resident in HBM before timing
+    X_bits, W_bits, Xc_bits = make_layer(w, index=list(WORKLOADS).index(args.workload))
+
+    def dev_bf16(b):
+        return torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).to(dev).view(torch.bfloat16)
+
+    X, W_full, Xc = dev_bf16(X_bits), dev_bf16(W_bits), dev_bf16(Xc_bits)
+    comm = None
+    if world > 1:
+        comm, _, _ = rrs.make_comm()
+    stream = torch.cuda.current_stream()
+    perm = rrs.calibrate_perm(Xc)                      # offline reorder (R5), on the GPU
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    layer = rrs.RRSLinear(W_full, perm, comm=comm, world=world, rank=rank)  # a7, offline
+    t1.record()
+    torch.cuda.synchronize()
+    prep_ms = t0.elapsed_time(t1)
+    del W_full
+    n_local = N // world
+    ws = torch.empty(rrs.rrs_workspace_bytes(T, N, K, 128, world), dtype=torch.uint8, device=dev)
+    Xq8 = torch.empty((T, K), dtype=torch.int8, device=dev)
+    xs = torch.empty(T, dtype=torch.float32, device=dev)
+    sg = torch.empty(K // 128, dtype=torch.float32, device=dev)
+    cm = torch.empty(K, dtype=torch.float32, device=dev)
+    Y_shard = torch.empty((T, n_local), dtype=out_dtype, device=dev)
+    Y = torch.empty((T, N), dtype=out_dtype, device=dev) if world > 1 else Y_shard
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    out_scale = 1.0 / K
+
+    def step(ev):
+        ev[0].record(stream)
+        rrs.rrs_rotate_smooth_quant(X, perm, None, Xq8, xs, sg, chan_max=cm, stream=stream)
+        ev[1].record(stream)
+        rrs.rrs_gemm(Xq8, xs, sg, layer.Wq8, layer.w_scale, Y_shard, out_scale, stream=stream)
+        ev[2].record(stream)
+        if world > 1:
+            rrs.rrs_allgather_columns(Y_shard, Y, comm, ws, stream=stream)
+        ev[3].record(stream)
+
+    def plain_gemm(ev):
+        ev[0].record(stream)
+        rrs.rrs_gemm(Xq8, xs, None, layer.Wq8, layer.w_scale, Y_shard, out_scale, plain=True, stream=stream)
+        ev[1].record(stream)
+
+    def new_events(n, k):
+        return [[torch.cuda.Event(enable_timing=True) for _ in range(k)] for _ in range(n)]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step(new_events(1, 4)[0])
+    barrier()
+    evs = new_events(args.steps, 4)
+    with ClockSampler(local) as clocks:
+        barrier()
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()
+            step(evs[i])
+        barrier()
+        wall = time.perf_counter() - wall0
+    per_step = [evs[i][0].elapsed_time(evs[i][3]) for i in range(args.steps)]
+    prologue = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
+    gemm = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
+    gather = [evs[i][2].elapsed_time(evs[i][3]) for i in range(args.steps)]
+
+    # plain per-channel A4W4 GEMM on the same operands (the paper's overhead baseline)
+    pev = new_events(args.steps, 2)
+    for i in range(args.steps):
+        flush.zero_()
+        plain_gemm(pev[i])
+    torch.cuda.synchronize()
+    plain = [pev[i][0].elapsed_time(pev[i][1]) for i in range(args.steps)]
+
+    # end to end through the public API with host buffers: pinned H2D of X, rrs_linear, D2H of Y
+    X_host = X.cpu().pin_memory()
+    Y_host = torch.empty((T, N), dtype=out_dtype).pin_memory()
+    X_dev = torch.empty_like(X)
+    Y_e2e = torch.empty((T, N), dtype=out_dtype, device=dev)
+    lin_ws = layer.workspace(T, dev)
+    eev = new_events(args.steps, 2)
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        ev = eev[i - args.warmup] if i >= args.warmup else new_events(1, 2)[0]
+        ev[0].record(stream)
+        X_dev.copy_(X_host, non_blocking=True)
+        rrs.rrs_linear(X_dev, perm, layer.Wq8, layer.w_scale, Y_e2e, lin_ws, N_total=N, comm=comm, stream=stream)
+        Y_host.copy_(Y_e2e, non_blocking=True)
+        ev[1].record(stream)
+    torch.cuda.synchronize()
+    e2e = [eev[i][0].elapsed_time(eev[i][1]) for i in range(args.steps)]
+
+    def mx(vals):  # mean per rank, max over ranks
+        v = torch.tensor([statistics.fmean(vals)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(v, op=dist.ReduceOp.MAX)
+        return float(v.item())
+
+    ms_step, ms_pro, ms_gemm, ms_gather = mx(per_step), mx(prologue), mx(gemm), mx(gather)
+    ms_plain, ms_e2e = mx(plain), mx(e2e)
+    ck = clocks.summary()
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return None
+
+    ops = 2.0 * T * K * N
+    pk = peaks()
+    int8_peak = pk["bf16_tflops"] * INT8_OVER_BF16
+    gemm_tops = 2.0 * T * K * n_local / (ms_gemm * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get(args.workload, {}).get("gemm_dram_bytes_per_launch")
+    out = {
+        "metric": METRIC,
+        "value": ops / (ms_step * 1e-3) / 1e12,
+        "unit": "TOPS",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_step,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "int8",
+        "data": "synthetic (seeded LLaMA-like bf16 activations, N(0,0.02^2) bf16 weights; rrs_synth)",
+        "config": {"workload": args.workload, "T": T, "K": K, "N": N, "group": 128, "out_dtype": args.out_dtype,
+                   "parallelism": f"tp-columns x{world}" if world > 1 else "single",
+                   "l2": "flushed before every timed step (256 MiB write); per-step CUDA events"},
+        "tokens_per_s": T / (ms_step * 1e-3),
+        "breakdown_ms": {"prologue": ms_pro, "rrs_gemm": ms_gemm, "allgather": ms_gather,
+                         "plain_gemm": ms_plain, "prepare_weights_offline": prep_ms},
+        "gemm_tops": gemm_tops,
+        "gemm_pct_int8_peak": 100.0 * gemm_tops / int8_peak,
+        "rrs_overhead_vs_plain_gemm": ms_gemm / ms_plain - 1.0,
+        "roofline": {"bound": "tensor", "kernel": "rrs_gemm_kernel", "achieved": gemm_tops, "peak": int8_peak,
+                     "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
+                     "peak_src": f"int8 = {INT8_OVER_BF16:g} x bf16 burst {pk['bf16_tflops']} TFLOP/s, {pk['src']}",
+                     "algorithmic": "2*T*K*N_local int ops per launch (SURVEY §8(d))"},
+        "e2e": {"value": ops / (ms_e2e * 1e-3) / 1e12, "unit": "TOPS", "h2d_bytes_per_step": T * K * 2,
+                "d2h_bytes_per_step": T * N * esz, "api": "rrs_linear (pinned host X -> device -> host Y)"},
+        "gpu_launches": 3 + (1 if world > 1 else 0),
+        "clocks": ck,
+        "wall_s_timed_region": wall,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(w, X_bits, W_bits, Xc_bits, budget_s=args.cpu_budget)
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return out
+
+
+# ------------------------------------------------------------------------------------------ CPU oracle
+
+def _oracle_step(o, Xs, Wr_prepared, perm, K):
+    Xr = o.rotate(Xs)
+    c = o.channel_max(Xr)
+    s = o.group_scales(c, perm, 128)
+    q, a = o.smooth_quant(Xr, perm, s, 128)
+    qw, beta = Wr_prepared
+    return o.scale_accumulate_rows(q, qw, s, a, beta, 128, 1.0 / K)
+
+
+def cpu_baseline(w, X_bits, W_bits, Xc_bits, budget_s=20.0, rows=None):
+    """The oracle as it stands, timed on this host's cores on a bounded token sample of the workload."""
+    from oracle import rrs_oracle as o
+    from rrs_synth import bf16_bits_to_f64
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count()
+    perm = o.calibrate_perm(bf16_bits_to_f64(Xc_bits[:256]))
+    qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits), perm)  # offline, not timed
+    T = rows or min(w.T, 256)
+    Xs = bf16_bits_to_f64(X_bits[:T])
+    t = time.perf_counter()
+    n = 0
+    while True:
+        _oracle_step(o, Xs, (qw, beta), perm, w.K)
+        n += 1
+        if time.perf_counter() - t > budget_s / 2 or n >= 8:
+            break
+    dt = (time.perf_counter() - t) / n
+    return {"value": 2.0 * T * w.K * w.N / dt / 1e12, "unit": "TOPS", "cores": threads, "kind": "oracle",
+            "sample": f"{T} of {w.T} tokens of {w.name} (K={w.K}, N={w.N}), full layer forward a1-a9 "
+                      f"(weights prepared offline, untimed), {n} repetitions, {dt:.2f} s each"}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle as the reference arm (rank 0 only; other ranks exit 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    from oracle import rrs_oracle as o
+    from rrs_synth import bf16_bits_to_f64
+    w = WORKLOADS[args.workload]
+    X_bits, W_bits, Xc_bits = make_layer(w, index=list(WORKLOADS).index(args.workload))
+    perm = o.calibrate_perm(bf16_bits_to_f64(Xc_bits[:256]))
+    qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits), perm)
+    T = min(w.T, args.ref_rows)
+    Xs = bf16_bits_to_f64(X_bits[:T])
+    for _ in range(args.warmup):
+        _oracle_step(o, Xs, (qw, beta), perm, w.K)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        _oracle_step(o, Xs, (qw, beta), perm, w.K)
+        times.append(time.perf_counter() - t)
+    dt = statistics.fmean(times)
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count()
+    value = 2.0 * T * w.K * w.N / dt / 1e12
+    sample = f"{T} of {w.T} tokens of {w.name} per step (K={w.K}, N={w.N}), layer forward a1-a9"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "TOPS", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (rrs_synth)",
+           "config": {"workload": args.workload, "T": w.T, "K": w.K, "N": w.N, "group": 128,
+                      "sample_tokens": T},
+           "cpu_baseline": {"value": value, "unit": "TOPS", "cores": threads, "kind": "oracle", "sample": sample},
+           "e2e": {"value": value, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["rrs", "reference"], default="rrs")
+    ap.add_argument("--workload", default="c2_llama2_7b_qo", choices=sorted(WORKLOADS))
+    ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--ref-rows", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -122,6 +122,12 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
                       void* Y, int32_t y_dtype, int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes,
                       void* stream);
 
+/* The collective step of the column-parallel layer on its own: all-gather every rank's
+ * Y shard [T][N_total/world] (contiguous, y_dtype) over NCCL and re-lay it out into Y[T][ldy]
+ * (rank r's shard -> columns [r*N_total/world, (r+1)*N_total/world)).  ws as for rrs_linear. */
+rrs_status rrs_allgather_columns(const void* Y_shard, int64_t T, int64_t N_total, int32_t y_dtype, void* Y,
+                                 int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, void* stream);
+
 /* Communicator (NCCL over NVLink/NVSwitch).  torch.distributed only ferries the 128-byte id. */
 rrs_status rrs_comm_unique_id(uint8_t id[128]);
 rrs_status rrs_comm_init(rrs_comm_t* comm, int32_t rank, int32_t world, const uint8_t id[128]);

@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import torch
 
-from ._lib import (EXPORTS, RRSError, lib, rrs_comm_destroy, rrs_comm_init, rrs_comm_unique_id,  # noqa: F401
+from ._lib import (EXPORTS, RRSError, lib, rrs_allgather_columns, rrs_comm_destroy, rrs_comm_init, rrs_comm_unique_id,  # noqa: F401
                    rrs_debug_group_partials, rrs_debug_rotate, rrs_gemm, rrs_linear, rrs_perm_from_channel_max,
                    rrs_prepare_weights, rrs_rotate_smooth_quant, rrs_version, rrs_workspace_bytes)
 

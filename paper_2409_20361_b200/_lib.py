@@ -35,6 +35,7 @@ _SIGS = {
                                 _c_p, _c_i32, _c_i64, _c_p]),
     "rrs_linear": (ctypes.c_int, [_c_p, _c_i32, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_i32,
                                   _c_i64, _c_p, _c_p, _c_sz, _c_p]),
+    "rrs_allgather_columns": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_i64, _c_p, _c_p, _c_sz, _c_p]),
     "rrs_comm_unique_id": (ctypes.c_int, [_c_p]),
     "rrs_comm_init": (ctypes.c_int, [ctypes.POINTER(_c_p), _c_i32, _c_i32, _c_p]),
     "rrs_comm_destroy": (ctypes.c_int, [_c_p]),
@@ -157,6 +158,14 @@ def rrs_linear(X, perm, Wq8, w_scale, Y, ws, N_total: int | None = None, comm=No
            lib().rrs_linear(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Wq8), _ptr(w_scale), N_total,
                             _ptr(Y, True), _y_code(Y), Y.stride(0), comm, _ptr(ws), ws.numel() * ws.element_size(),
                             _stream(stream)))
+
+
+def rrs_allgather_columns(Y_shard, Y, comm, ws, stream=None) -> None:
+    T = Y_shard.shape[0]
+    N_total = Y.shape[1]
+    _check("rrs_allgather_columns",
+           lib().rrs_allgather_columns(_ptr(Y_shard), T, N_total, _y_code(Y_shard), _ptr(Y, True), Y.stride(0), comm,
+                                       _ptr(ws), ws.numel() * ws.element_size(), _stream(stream)))
 
 
 def rrs_comm_unique_id() -> bytes:

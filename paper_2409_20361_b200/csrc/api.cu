@@ -118,6 +118,19 @@ struct rrs_comm_s {
   int rank, world;
 };
 
+static rrs_status gather_columns(const void* shard, int64_t T, int64_t N_total, int esz, void* Y, int64_t ldy,
+                                 rrs_comm_t comm, void* gather_buf, cudaStream_t st) {
+  const int world = comm->world;
+  const int64_t n_local = N_total / world;
+  if ((n_local * esz) % 16 || (ldy * esz) % 16)
+    return fail(RRS_ERR_MISALIGNED, "shard width and ldy must be multiples of 16 bytes");
+  ncclResult_t r = ncclAllGather(shard, gather_buf, (size_t)T * n_local * esz, ncclUint8, comm->nccl, st);
+  if (r != ncclSuccess) return fail(RRS_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
+  cudaError_t e = rrs::launch_relayout_shards(gather_buf, Y, T, n_local, world, ldy, esz, st);
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "relayout kernel");
+}
+
+
 extern "C" {
 
 const char* rrs_status_str(int s) {
@@ -267,10 +280,25 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, n_local, K, group, out_scale, false, w.y_shard, y_dtype, n_local, nullptr};
   cudaError_t e = rrs::launch_gemm(a, nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "rrs_gemm kernel");
-  ncclResult_t r = ncclAllGather(w.y_shard, w.y_gather, (size_t)T * n_local * esz, ncclUint8, comm->nccl, st);
-  if (r != ncclSuccess) return fail(RRS_ERR_NCCL, "ncclAllGather: %s", ncclGetErrorString(r));
-  e = rrs::launch_relayout_shards(w.y_gather, Y, T, n_local, world, ldy, esz, st);
-  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "relayout kernel");
+  return gather_columns(w.y_shard, T, N_total, esz, Y, ldy, comm, w.y_gather, st);
+}
+
+rrs_status rrs_allgather_columns(const void* Y_shard, int64_t T, int64_t N_total, int32_t y_dtype, void* Y,
+                                 int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, void* stream) {
+  g_last_error.clear();
+  if (!comm) return fail(RRS_ERR_INVALID_ARGUMENT, "comm is NULL");
+  if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
+  if (T < 0 || N_total < 1 || N_total % comm->world || ldy < N_total)
+    return fail(RRS_ERR_INVALID_ARGUMENT, "shape");
+  if (T == 0) return RRS_OK;
+  if (!Y_shard || !Y || !aligned16(Y_shard) || !aligned16(Y) || !aligned16(ws))
+    return fail(RRS_ERR_MISALIGNED, "pointers");
+  Workspace w;
+  // any K with a valid carve works: the gather buffer only depends on T and N
+  const size_t need = carve(ws, T, N_total, 128, 128, comm->world, &w);
+  if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
+  return gather_columns(Y_shard, T, N_total, y_dtype == RRS_F32 ? 4 : 2, Y, ldy, comm, w.y_gather,
+                        static_cast<cudaStream_t>(stream));
 }
 
 rrs_status rrs_comm_unique_id(uint8_t id[128]) {

@@ -26,6 +26,10 @@ def _perm(Xc_bits):
     return o.calibrate_perm(bf16_bits_to_f64(Xc_bits)).astype(np.int32)
 
 
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
 def _u32(t):
     return t.cpu().numpy().view(np.uint32)
 
@@ -150,8 +154,8 @@ def _gemm_case(T, N, K, profile="channel", seed=0):
                                            (64, 512, 8192, "mixed")])
 def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile):
     X_bits, W_bits, perm, ref = _gemm_case(T, N, K, profile)
-    Xq8 = torch.from_numpy(ref["q"]).to(DEV)
-    Wq8 = torch.from_numpy(ref["qw"]).to(DEV)
+    Xq8 = _dev(ref["q"])
+    Wq8 = _dev(ref["qw"])
     xs = torch.from_numpy(ref["alpha"]).to(DEV)
     sg = torch.from_numpy(ref["s_group"]).to(DEV)
     ws = torch.from_numpy(ref["beta"]).to(DEV)
@@ -170,8 +174,8 @@ def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile):
 def test_plain_gemm_matches_per_channel_baseline():
     """RRS_GEMM_PLAIN: Y = alpha beta sum_all q qw / K (per-channel A4W4)."""
     X_bits, W_bits, perm, ref = _gemm_case(130, 300, 1024)
-    Xq8 = torch.from_numpy(ref["q"]).to(DEV)
-    Wq8 = torch.from_numpy(ref["qw"]).to(DEV)
+    Xq8 = _dev(ref["q"])
+    Wq8 = _dev(ref["qw"])
     Y = torch.empty((130, 304), dtype=torch.float32, device=DEV)
     rrs.rrs_gemm(Xq8, torch.from_numpy(ref["alpha"]).to(DEV), None, Wq8, torch.from_numpy(ref["beta"]).to(DEV),
                  Y[:, :300], 1.0 / 1024, plain=True)
