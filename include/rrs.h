@@ -65,7 +65,8 @@ const char* rrs_last_error(void);
 int rrs_version(void);
 
 /* Workspace bytes needed by rrs_linear / rrs_rotate_smooth_quant for T tokens:
- * chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xq8[T][K] int8 (+ Y shard and gather
+ * X~[T][K] f32 (the rotated activation, written once by the FWHT pass and read by the quantisation
+ * pass) + chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xq8[T][K] int8 (+ Y shard and gather
  * buffers when world > 1), each 256-byte aligned.  Returns 0 for invalid arguments. */
 size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world);
 
@@ -81,7 +82,8 @@ rrs_status rrs_perm_from_channel_max(const float* chan_max, int64_t K, int32_t* 
  *   beta_n = fl(max_j |W~_nj| / 7) (1 if the row is zero, R8); codes rint_even(fl(W~ * fl(7/max))).
  * W: device bf16 bits [N][K].  perm: device int32 [K] (NULL = identity is NOT accepted: pass it).
  * Outputs (device, caller-owned; Wq and Wq8 may each be NULL but not both):
- *   Wq  uint8 [N][K/2] packed INT4;  Wq8 int8 [N][K] GEMM operand;  w_scale f32 [N] = beta_n. */
+ *   Wq  uint8 [N][K/2] packed INT4;  Wq8 int8 [N][K] GEMM operand;  w_scale f32 [N] = beta_n.
+ * Offline helper: it takes a stream-ordered temporary (cudaMallocAsync, <= 256 MiB) for the rotated rows. */
 rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_t K, int32_t group,
                                const int32_t* perm, uint8_t* Wq, int8_t* Wq8, float* w_scale,
                                void* stream);
@@ -95,7 +97,7 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
  * X: device bf16 bits [T][K]; perm: device int32 [K];
  * outputs: Xq uint8 [T][K/2] (nullable), Xq8 int8 [T][K] (nullable), x_scale f32 [T],
  *          s_group f32 [K/group], chan_max f32 [K] (nullable: then taken from ws).
- * ws: device scratch (>= rrs_workspace_bytes(T, 1, K, group, 1) when chan_max == NULL, else may be NULL). */
+ * ws: device scratch, 16-byte aligned, >= rrs_workspace_bytes(T, 1, K, group, 1) bytes (holds X~). */
 rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
                                    const int32_t* perm, uint8_t* Xq, int8_t* Xq8, float* x_scale,
                                    float* s_group, float* chan_max, void* ws, size_t ws_bytes,

@@ -134,6 +134,8 @@ def rrs_prepare_weights(W, perm, Wq, Wq8, w_scale, group: int = 128, stream=None
 def rrs_rotate_smooth_quant(X, perm, Xq, Xq8, x_scale, s_group, chan_max=None, ws=None, group: int = 128,
                             stream=None) -> None:
     T, K = X.shape
+    if ws is None:  # marshalling convenience: torch owns the scratch (X~ f32 + chan_max), see rrs_workspace_bytes
+        ws = torch.empty(rrs_workspace_bytes(T, 1, K, group, 1), dtype=torch.uint8, device=X.device)
     _check("rrs_rotate_smooth_quant",
            lib().rrs_rotate_smooth_quant(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Xq), _ptr(Xq8),
                                          _ptr(x_scale), _ptr(s_group), _ptr(chan_max), _ptr(ws),

@@ -1,4 +1,5 @@
 // C-ABI host layer of librrs (include/rrs.h): validation, workspace carving, launches, NCCL comm.
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -80,6 +81,7 @@ rrs_status check_shape(int64_t T, int64_t K, int32_t group) {
 }
 
 struct Workspace {
+  float* Xr;        // rotated activation X~ f32 [T][K] (written once by the FWHT pass, read by the quant pass)
   float* chan_max;
   float* s_group;
   float* x_scale;
@@ -97,6 +99,7 @@ size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t
   };
   Workspace tmp;
   Workspace& ws = w ? *w : tmp;
+  ws.Xr = static_cast<float*>(take(sizeof(float) * (size_t)T * K));
   ws.chan_max = static_cast<float*>(take(sizeof(float) * K));
   ws.s_group = static_cast<float*>(take(sizeof(float) * (K / group)));
   ws.x_scale = static_cast<float*>(take(sizeof(float) * (T > 0 ? T : 1)));
@@ -177,21 +180,35 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
   if (!W || !perm || !w_scale || (!Wq && !Wq8)) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned16(W) || !aligned16(perm) || !aligned16(Wq) || !aligned16(Wq8))
     return fail(RRS_ERR_MISALIGNED, "pointers must be 16-byte aligned");
-  cudaError_t e = rrs::launch_fwht_quant(static_cast<const uint16_t*>(W), N, K, perm, nullptr, nullptr, Wq, Wq8,
-                                         w_scale, nsm, static_cast<cudaStream_t>(stream));
-  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "fwht_quant_kernel (weights)");
+  // offline path: rotate a chunk of rows into a stream-ordered temporary, then quantise it per row
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t(256) << 20) / (K * 4)));
+  float* tmp = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(float) * chunk * K, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (weight rotation scratch)");
+  const uint16_t* Wb = static_cast<const uint16_t*>(W);
+  for (int64_t n0 = 0; n0 < N && e == cudaSuccess; n0 += chunk) {
+    const int64_t rows = std::min(chunk, N - n0);
+    e = rrs::launch_fwht_colmax(Wb + n0 * K, rows, K, nullptr, tmp, nsm, st);
+    if (e == cudaSuccess)
+      e = rrs::launch_smooth_quant(tmp, rows, K, perm, nullptr, nullptr, Wq ? Wq + n0 * (K / 2) : nullptr,
+                                   Wq8 ? Wq8 + n0 * K : nullptr, w_scale + n0, nsm, st);
+  }
+  cudaError_t e2 = cudaFreeAsync(tmp, st);
+  if (e != cudaSuccess) return cuda_fail(e, "weight preparation kernels");
+  return e2 == cudaSuccess ? RRS_OK : cuda_fail(e2, "cudaFreeAsync");
 }
 
 static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* perm, uint8_t* Xq, int8_t* Xq8,
-                           float* x_scale, float* s_group, float* chan_max, int nsm, cudaStream_t st) {
+                           float* x_scale, float* s_group, float* chan_max, float* Xr, int nsm, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * K, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
-  e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), nullptr,
+  e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
                               nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "fwht_colmax_kernel");
-  e = rrs::launch_fwht_quant(static_cast<const uint16_t*>(X), T, K, perm, reinterpret_cast<const unsigned*>(chan_max),
-                             s_group, Xq, Xq8, x_scale, nsm, st);
-  if (e != cudaSuccess) return cuda_fail(e, "fwht_quant_kernel");
+  e = rrs::launch_smooth_quant(Xr, T, K, perm, reinterpret_cast<const unsigned*>(chan_max), s_group, Xq, Xq8,
+                               x_scale, nsm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "smooth_quant_kernel");
   return RRS_OK;
 }
 
@@ -207,13 +224,12 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
     return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!aligned16(X) || !aligned16(perm) || !aligned16(Xq) || !aligned16(Xq8))
     return fail(RRS_ERR_MISALIGNED, "pointers must be 16-byte aligned");
-  if (!chan_max) {
-    Workspace w;
-    const size_t need = carve(ws, T, 1, K, group, 1, &w);
-    if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
-    chan_max = w.chan_max;
-  }
-  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, nsm, static_cast<cudaStream_t>(stream));
+  Workspace w;
+  const size_t need = carve(ws, T, 1, K, group, 1, &w);
+  if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
+  if (!aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "workspace must be 16-byte aligned");
+  if (!chan_max) chan_max = w.chan_max;
+  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, w.Xr, nsm, static_cast<cudaStream_t>(stream));
 }
 
 static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int8_t* Wq8, const float* w_scale,
@@ -264,7 +280,8 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, nsm, st)) return s;
+  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, w.Xr, nsm, st))
+    return s;
   if (T == 0) return RRS_OK;
   const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
   const int esz = y_dtype == RRS_F32 ? 4 : 2;

@@ -1,59 +1,62 @@
-// FP64-exact fast Walsh-Hadamard transform of bf16 rows for sm_100a.
+// FP64-exact fast Walsh-Hadamard transform of bf16 rows for sm_100a (SURVEY.md §8 row a1).
 //
 // Computes X~ = X . H_K per row (Eq. 4; App. A.1) with the
 // UNNORMALISED +-1 matrix H (R1: the 1/K = (1/sqrt K)^2 goes to the GEMM epilogue).
 //   K = 2^m      : Sylvester H, butterflies over the bits of the column index.
-//   K = 28 * 2^m : H28 (x) H_{2^m} (R2): FWHT-2^m on the 28 contiguous chunks, then the
-//                  structured Paley-II H28 mix across chunks (S (x) A2 + I14 (x) B2, 16 adds/elem).
+//   K = 28 * 2^m : H28 (x) H_{2^m} (R2): FWHT-2^m inside each of the 28 contiguous chunks, then
+//                  the structured Paley-II H28 mix across chunks (S (x) A2 + I14 (x) B2).
 // Every intermediate is a signed subset sum of the row's inputs, hence exact in float64 under the
-// exactness precondition (R3); the single final __double2float_rn gives the correctly
-// rounded f32 value, bit-identical to the oracle's f32_rne(sum).
+// exactness precondition (R3); the single final __double2float_rn gives the correctly rounded
+// f32 value, bit-identical to the oracle's f32_rne(sum).  The butterfly stages commute, so they may be
+// run in any bit order.
 //
-// Data movement: a CTA owns R rows at a time.  Pass A loads 32 contiguous bf16 per thread straight
-// from HBM (4 x 16-byte loads) and runs 5 butterfly stages in registers; each further pass goes
-// through shared memory (XOR swizzle p(i) = i ^ ((i>>5)&15) keeps every warp access at the
-// 2-wavefront minimum for doubles) and runs up to 5 more stages in registers.
+// Data movement: every thread holds 64 doubles.  Pass 0 covers index bits {0,1,2} and the
+// top three bits of the 2^m part, so a thread's inputs are 8 chunks of 8 contiguous bf16 (16-byte loads,
+// coalesced across threads).  Each later pass covers the next (up to) 6 middle bits after one trip through
+// shared memory; the H28 mix is one more pass.  K = 4096 therefore needs a single transpose (16 B of
+// shared-memory traffic per element against 12 DADDs): the kernel is FP64-pipe bound.  swz() keeps the
+// pass-0 stores (stride 8) and the pass-1 accesses (runs of 8, stride 512) at the 2-wavefront minimum.
 #pragma once
 #include "common.cuh"
 
 namespace rrs {
 
-constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
-constexpr int max_c(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2_c(n >> 1); }
+__host__ __device__ constexpr int max_c(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int min_c(int a, int b) { return a < b ? a : b; }
 
 template <int K_>
 struct FwhtPlan {
   static constexpr int K = K_;
   static constexpr bool kPow2 = (K & (K - 1)) == 0;
-  static constexpr int A = kPow2 ? 1 : 28;
-  static constexpr int N = K / A;             // power-of-two part
-  static constexpr int LOGN = ilog2_c(N);
-  static constexpr int E = 32;                // elements per thread in the 2^m passes
-  static constexpr int TPR = K / E;           // threads per row in the 2^m passes
-  static constexpr int H28T = kPow2 ? 0 : N;  // threads of the H28 pass (28 elements each)
-  static constexpr int CTA = max_c(256, max_c(TPR, H28T));
-  static constexpr int R = kPow2 ? CTA / TPR : 1;  // rows per CTA iteration
-  static constexpr int SLOTS = kPow2 ? 32 : 28;    // values per thread after the last pass
-  static constexpr int SMEM_BYTES = R * K * 8 + 64 * 4;  // double tile + reduction scratch
-  static_assert(A * N == K, "K must be 2^m or 28*2^m");
-  static_assert((N & (N - 1)) == 0 && N >= 32, "power-of-two part must be >= 32");
+  static constexpr int A = kPow2 ? 1 : 28;          // H28 factor
+  static constexpr int NP2 = K / A;                  // power-of-two part
+  static constexpr int LOGN = ilog2_c(NP2);
+  static constexpr int TP2 = K / 64;                 // threads per row in the 2^m passes (64 values each)
+  static constexpr int TH28 = kPow2 ? 0 : NP2 / 2;   // threads per row in the H28 pass (2 groups of 28)
+  static constexpr int TPR = max_c(TP2, TH28);       // threads per row
+  static constexpr int R = kPow2 ? max_c(1, 64 / TP2) : 1;  // rows per CTA tile (>= 2 warps per CTA)
+  static constexpr int THREADS = ((R * TPR + 31) / 32) * 32;
+  static constexpr int HI = LOGN - 3;                // pass 0: bits [0,3) and [HI, LOGN)
+  static constexpr int SLOTS = kPow2 ? 64 : 56;      // values per thread after the last pass
+  static constexpr int TILE = R * K;                 // elements per CTA tile
+  static_assert(A * NP2 == K, "K must be 2^m or 28*2^m");
+  static_assert(LOGN >= 7, "power-of-two part must be >= 128");
   static_assert(K % 128 == 0, "K must be a multiple of the group size 128");
-  static_assert(CTA <= 1024, "K too large for one CTA");
-  // last 2^m pass covers bits [LAST_B, LOGN)
-  static constexpr int NUM_POW2_PASSES = (LOGN + 4) / 5;
-  static constexpr int LAST_B = (NUM_POW2_PASSES - 1) * 5;
-  static constexpr int LAST_R = LOGN - LAST_B;
+  static_assert(THREADS <= 1024, "K too large for one CTA");
+  static_assert(kPow2 || TP2 <= TH28, "H28 layout");
 };
 
-RRS_DEVICE int swz(int i) { return i ^ ((i >> 5) & 15); }
+// bijective on any tile (XORs bits 0-3 with functions of bits >= 4)
+RRS_DEVICE int swz(int i) { return i ^ ((i >> 4) & 7) ^ (((i >> 9) & 1) << 3); }
 
-// radix-2^r butterflies over groups v[u*2^r + k], u < 32>>r  (all stages of the pass in registers)
-template <int r, int SZ>
-RRS_DEVICE void butterflies(double (&v)[SZ]) {
+// radix-2^r butterflies over the groups v[u*2^r + k], u < 64 >> r (all stages of a pass in registers)
+template <int r>
+RRS_DEVICE void butterflies(double (&v)[64]) {
 #pragma unroll
   for (int h = 1; h < (1 << r); h <<= 1) {
 #pragma unroll
-    for (int u = 0; u < (SZ >> r); ++u) {
+    for (int u = 0; u < (64 >> r); ++u) {
 #pragma unroll
       for (int k = 0; k < (1 << r); ++k) {
         if ((k & h) == 0) {
@@ -66,34 +69,39 @@ RRS_DEVICE void butterflies(double (&v)[SZ]) {
   }
 }
 
-// element index (within the R-row tile) of element k of group (tid, u) in the pass over bits [b, b+r)
+// Row-local index of register j = kh*8 + kl of row-thread tp in pass 0.
+template <class P>
+RRS_DEVICE int p0_index(int tp, int j) {
+  constexpr int per_chunk = P::NP2 / 64;  // threads per 2^m chunk
+  const int a = tp / per_chunk, t = tp % per_chunk;
+  return a * P::NP2 + ((j >> 3) << P::HI) + (t << 3) + (j & 7);
+}
+
+// Row-local index of element k of group u of row-thread tp in the pass over the middle bits [b, b+r).
 template <class P, int b, int r>
-RRS_DEVICE int pass_index(int tid, int u, int k) {
-  const int g = tid + (P::R * P::TPR) * u;
-  const int gbits = P::LOGN - r;
-  const int o = g >> gbits;
-  const int gx = g & ((1 << gbits) - 1);
-  const int x = (gx & ((1 << b) - 1)) | (k << b) | ((gx >> b) << (b + r));
-  return (o << P::LOGN) | x;
+RRS_DEVICE int p2_index(int tp, int u, int k) {
+  const int g = tp + P::TP2 * u;  // the other bits, in [0, K / 2^r)
+  return (g & ((1 << b) - 1)) | (k << b) | ((g >> b) << (b + r));
 }
 
 // Paley-II H28 = S (x) [[1,-1],[-1,-1]] + I14 (x) [[1,1],[1,-1]], S = [[0,1^T],[1,Q]], Q_ij = chi13(j-i).
-// y = H28 . v  (H28 is symmetric, so row-vector x H28 == H28 x).
-RRS_DEVICE int chi13(int a) {
+// y = H28 . v (H28 is symmetric, so the row-vector product x H28 equals H28 x).
+RRS_DEVICE constexpr int chi13(int a) {
   a = ((a % 13) + 13) % 13;
   // quadratic residues mod 13: {1, 3, 4, 9, 10, 12}
   return a == 0 ? 0 : ((a == 1 || a == 3 || a == 4 || a == 9 || a == 10 || a == 12) ? 1 : -1);
 }
 
-RRS_DEVICE void h28_apply(double (&v)[28]) {
+template <int OFF>
+RRS_DEVICE void h28_apply(double (&v)[64]) {
   double u0[14], u1[14], w0[14], w1[14];
 #pragma unroll
   for (int i = 0; i < 14; ++i) {
-    const double x0 = v[2 * i], x1 = v[2 * i + 1];
-    u0[i] = x0 - x1;      // A2 row 0: ( 1, -1)
-    u1[i] = -x0 - x1;     // A2 row 1: (-1, -1)
-    w0[i] = x0 + x1;      // B2 row 0: ( 1,  1)
-    w1[i] = x0 - x1;      // B2 row 1: ( 1, -1)
+    const double x0 = v[OFF + 2 * i], x1 = v[OFF + 2 * i + 1];
+    u0[i] = x0 - x1;   // A2 row 0: ( 1, -1)
+    u1[i] = -x0 - x1;  // A2 row 1: (-1, -1)
+    w0[i] = x0 + x1;   // B2 row 0: ( 1,  1)
+    w1[i] = x0 - x1;   // B2 row 1: ( 1, -1)
   }
 #pragma unroll
   for (int j = 0; j < 14; ++j) {
@@ -104,100 +112,116 @@ RRS_DEVICE void h28_apply(double (&v)[28]) {
       const int sg = (j == 0 || i == 0) ? 1 : chi13((i - 1) - (j - 1));
       if (sg > 0) { s0 += u0[i]; s1 += u1[i]; } else { s0 -= u0[i]; s1 -= u1[i]; }
     }
-    v[2 * j] = s0;
-    v[2 * j + 1] = s1;
+    v[OFF + 2 * j] = s0;
+    v[OFF + 2 * j + 1] = s1;
   }
 }
 
-// 2^m passes over bits [b, b+r), r = min(5, LOGN-b), through shared memory; the last one leaves
-// its results in registers (and writes them back only if the H28 pass still has to read them).
-template <class P, int b>
-RRS_DEVICE void fwht_pow2_passes(double* sm, double (&v)[32]) {
-  if constexpr (b < P::LOGN) {
-    constexpr int r = (P::LOGN - b) < 5 ? (P::LOGN - b) : 5;
-    constexpr bool last = (b + r == P::LOGN);
-    const int tid = threadIdx.x;
-    __syncthreads();
-    if (tid < P::R * P::TPR) {
-#pragma unroll
-      for (int u = 0; u < (32 >> r); ++u)
-#pragma unroll
-        for (int k = 0; k < (1 << r); ++k) v[(u << r) + k] = sm[swz(pass_index<P, b, r>(tid, u, k))];
-      butterflies<r>(v);
-      if (!last || P::A == 28) {
-#pragma unroll
-        for (int u = 0; u < (32 >> r); ++u)
-#pragma unroll
-          for (int k = 0; k < (1 << r); ++k) sm[swz(pass_index<P, b, r>(tid, u, k))] = v[(u << r) + k];
-      }
-    }
-    fwht_pow2_passes<P, b + r>(sm, v);
-  }
-}
+// ------------------------------------------------------------------------------ pass plumbing
+// A "layout" names which index each register holds: pass 0 (L = -1), a middle pass starting at bit b
+// (L = b), or the H28 pass (L = -2).
 
-// Transform rows [r0, r0+R) of X (row stride ldx elements, bf16 bits) into v[] (double).
-// Rows >= T read as zero.  Ends with every thread holding SLOTS values; slot_rc() maps them.
-// Contains __syncthreads(): every thread of the CTA must call it.
-template <class P>
-RRS_DEVICE void fwht_tile(const uint16_t* __restrict__ X, int64_t ldx, int64_t T, int64_t r0,
-                          double* sm, double (&v)[32]) {
-  const int tid = threadIdx.x;
-  // ---- pass A: HBM -> registers, bits [0,5) ----
-  if (tid < P::R * P::TPR) {
-    const int rr = tid / P::TPR, tt = tid % P::TPR;
-    const int64_t row = r0 + rr;
-    if (row < T) {
-      const uint4* src = reinterpret_cast<const uint4*>(X + row * ldx + tt * 32);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 w = __ldg(src + q);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          v[q * 8 + 2 * h] = bf16_bits_to_double(ws[h] & 0xFFFFu);
-          v[q * 8 + 2 * h + 1] = bf16_bits_to_double(ws[h] >> 16);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < 32; ++k) v[k] = 0.0;
-    }
-    butterflies<(P::LOGN < 5 ? P::LOGN : 5)>(v);
-    if (P::NUM_POW2_PASSES > 1 || P::A == 28) {
-      const int base = rr * P::K + tt * 32;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) sm[swz(base + k)] = v[k];
-    }
-  }
-  fwht_pow2_passes<P, 5>(sm, v);
-  if constexpr (P::A == 28) {
-    __syncthreads();
-    // ---- H28 pass: thread x < N mixes the 28 chunk values at column offset x ----
-    double w[28];
-#pragma unroll
-    for (int a = 0; a < 28; ++a) w[a] = sm[swz(a * P::N + tid)];
-    h28_apply(w);
-#pragma unroll
-    for (int a = 0; a < 28; ++a) v[a] = w[a];
-  }
-}
-
-// (row within tile, column) of slot s of thread tid after fwht_tile
-template <class P>
-RRS_DEVICE void slot_rc(int tid, int s, int& row, int& col) {
-  if constexpr (P::A == 28) {
-    row = 0;
-    col = s * P::N + tid;
-  } else if constexpr (P::NUM_POW2_PASSES == 1) {
-    const int i = tid * 32 + s;
-    row = i / P::K;
-    col = i % P::K;
+template <class P, int L>
+RRS_DEVICE int reg_index(int tp, int j) {
+  if constexpr (L == -1) {
+    return p0_index<P>(tp, j);
+  } else if constexpr (L == -2) {
+    // group u (2 per thread) = column offset bb inside the 2^m chunk; register a = chunk index
+    return (j % 28) * P::NP2 + tp + P::TH28 * (j / 28);
   } else {
-    constexpr int b = P::LAST_B, r = P::LAST_R;
-    const int i = pass_index<P, b, r>(tid, s >> r, s & ((1 << r) - 1));
-    row = i / P::K;
-    col = i % P::K;
+    constexpr int r = min_c(6, P::HI - L);
+    return p2_index<P, L, r>(tp, j >> r, j & ((1 << r) - 1));
   }
+}
+
+template <class P, int L>
+RRS_DEVICE void store_layout(double* sm, int rr, int tp, const double (&v)[64]) {
+  constexpr int n = (L == -2) ? 56 : 64;
+#pragma unroll
+  for (int j = 0; j < n; ++j) sm[swz(rr * P::K + reg_index<P, L>(tp, j))] = v[j];
+}
+
+template <class P, int L>
+RRS_DEVICE void load_layout(const double* sm, int rr, int tp, double (&v)[64]) {
+  constexpr int n = (L == -2) ? 56 : 64;
+#pragma unroll
+  for (int j = 0; j < n; ++j) v[j] = sm[swz(rr * P::K + reg_index<P, L>(tp, j))];
+}
+
+// The middle passes [b, HI) following a pass with layout PL; finally the H28 pass.  Ends with v in the
+// layout last_layout<P>().  Every thread of the CTA must call it.
+template <class P, int PL, int b>
+RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, double (&v)[64]) {
+  if constexpr (b < P::HI) {
+    constexpr int r = min_c(6, P::HI - b);
+    if (p2act) store_layout<P, PL>(sm, rr, tp, v);
+    __syncthreads();
+    if (p2act) {
+      load_layout<P, b>(sm, rr, tp, v);
+      butterflies<r>(v);
+    }
+    __syncthreads();  // the tile is rewritten by the next pass (or by the next row)
+    fwht_rest<P, b, b + r>(sm, rr, tp, p2act, h28act, v);
+  } else if constexpr (!P::kPow2) {
+    if (p2act) store_layout<P, PL>(sm, rr, tp, v);
+    __syncthreads();
+    if (h28act) {
+      load_layout<P, -2>(sm, 0, threadIdx.x, v);  // H28 layout is indexed by the CTA thread
+      h28_apply<0>(v);
+      h28_apply<28>(v);
+    }
+    __syncthreads();
+  }
+}
+
+template <class P>
+__host__ __device__ constexpr int last_layout() {
+  if constexpr (!P::kPow2) return -2;
+  int b = 3, last = -1;
+  while (b < P::HI) {
+    last = b;
+    b += min_c(6, P::HI - b);
+  }
+  return last;
+}
+
+// Transform the R-row bf16 tile `stage` (shared memory, raw bits, row-major [R][K]) into v[].
+// Afterwards thread t holds, for j < SLOTS, the exact rotated value of row-local column
+// out_col<P>(tp, j) of tile row rr (t = rr * TP2 + tp in the 2^m passes; t = tp for H28).
+// active_rows masks rows beyond the matrix (their lanes still run, on whatever the stage holds).
+template <class P>
+RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[64], int& rr, int& tp) {
+  const int t = threadIdx.x;
+  const bool p2act = t < P::R * P::TP2;
+  const bool h28act = !P::kPow2 && t < P::TH28;
+  rr = P::kPow2 ? (p2act ? t / P::TP2 : 0) : 0;
+  const int tp2 = p2act ? t % P::TP2 : 0;
+  if (p2act) {
+    const uint16_t* row = stage + rr * P::K;
+#pragma unroll
+    for (int kh = 0; kh < 8; ++kh) {
+      const uint4 w = *reinterpret_cast<const uint4*>(row + p0_index<P>(tp2, kh * 8));
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        v[kh * 8 + 2 * h] = bf16_bits_to_double(ws[h] & 0xFFFFu);
+        v[kh * 8 + 2 * h + 1] = bf16_bits_to_double(ws[h] >> 16);
+      }
+    }
+    butterflies<6>(v);
+  }
+  fwht_rest<P, -1, 3>(sm, rr, tp2, p2act, h28act, v);
+  tp = P::kPow2 ? tp2 : t;
+}
+
+template <class P>
+RRS_DEVICE int out_col(int tp, int j) {
+  return reg_index<P, last_layout<P>()>(tp, j);
+}
+
+template <class P>
+RRS_DEVICE bool out_active(int t) {
+  return P::kPow2 ? t < P::R * P::TP2 : t < P::TH28;
 }
 
 }  // namespace rrs

@@ -5,15 +5,18 @@
 //                                                                     applied to the dequantized interim
 //                                                                     result"; R14, R15)
 //
-// Design (DESIGN.md §5): persistent, one CTA per SM, 320 threads = 10 warps:
+// Design (DESIGN.md §7): persistent, one CTA per SM, 320 threads = 10 warps:
 //   warp 0      TMA producer: 128x128 int8 X tile + 256x128 int8 W tile per group into a 4-stage
 //               SMEM ring (SWIZZLE_128B: one 128-code group is exactly one 128-byte swizzle row);
 //   warp 1      TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer (M=128, N=256, K=32, 4 per
 //               group) into one of two 256-column int32 TMEM accumulators, alternating per group;
-//   warps 2-9   promotion/epilogue: tcgen05.ld the group's int32 partials (lane quadrant = warp % 4,
-//               column half = (warp-2)/4), convert exactly with the 1.5*2^23 magic bias (|P_g| <= 6272
-//               < 2^22), acc = fma(s_g, P_g, acc) in registers, release the TMEM buffer, and after the
-//               last group scale by alpha_t * beta_n * out_scale and store Y.
+//   warps 2-9   promotion/epilogue (lane quadrant = warp % 4, column half = (warp-2)/4: 128 columns,
+//               whose f32 accumulators stay in registers).
+// Exact int32 -> f32 with no integer instruction: every accumulator buffer is pre-loaded (tcgen05.st)
+// with the bit pattern of 1.5*2^23 and the MMAs always accumulate onto it, so the buffer holds the bits
+// of the float 1.5*2^23 + P_g, exact because |P_g| <= 6272 < 2^22 (and |sum_k| <= 702464 in plain mode).
+// Promotion per pair of outputs is then one packed FADD (-1.5*2^23, exact) and one packed FFMA
+// (acc += s_g * P_g) on the f32x2 path; after reading a buffer the warp re-stores the bias and releases it.
 // The MMA of group g+1 overlaps the promotion of group g (two TMEM buffers).  In plain mode (the
 // per-channel A4W4 baseline of P:322) the MMA accumulates all K into one buffer per tile instead.
 #include <algorithm>
@@ -34,7 +37,8 @@ constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;          // 16 KiB
 constexpr int B_BYTES = BN * BK;          // 32 KiB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NUM_EPI_WARPS = 8;
+constexpr int NUM_EPI_WARPS = 16;
+constexpr int EPI_COLS = BN / (NUM_EPI_WARPS / 4);  // columns per promotion thread (64)
 constexpr int THREADS = 64 + NUM_EPI_WARPS * 32;
 constexpr int MAX_G = 128;                 // K <= 16384
 constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 1024 /*barriers, scales*/ +
@@ -53,8 +57,8 @@ struct GemmParams {
   int32_t* P_debug;
 };
 
-template <bool kPlain, bool kF32Out>
-__global__ void __launch_bounds__(gemm::THREADS, 1)
+template <bool kPlain, bool kF32Out, bool kDebug>
+__global__ void __maxnreg__(112)
 rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                 GemmParams p) {
   using namespace gemm;
@@ -121,7 +125,8 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       for (int kb = 0; kb < p.G; ++kb) {
         const uint32_t b = acc_iter & 1;
         if (kPlain ? kb == 0 : true) {
-          ptx::mbar_wait(&tempty[b], ((acc_iter >> 1) & 1) ^ 1);
+          // use u = acc_iter >> 1 of buffer b needs the (u)-th bias store (completion #u of tempty[b])
+          ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
         }
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
@@ -131,9 +136,9 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           const uint32_t d = tmem_base + b * BN;
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
-            // advance 32 bytes (= 32 int8 codes) along K inside the 128-byte swizzle row
-            const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (k > 0);
-            ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
+            // advance 32 bytes (= 32 int8 codes) along K inside the 128-byte swizzle row; always
+            // accumulate: the buffer starts at the magic bias
+            ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
           }
           ptx::mma_commit(&empty[stage]);
           if (!kPlain || kb == p.G - 1) ptx::mma_commit(&tfull[b]);
@@ -145,64 +150,85 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     }
   } else {
     // ------------------------------------------------------------------ promotion + epilogue
-    const int ew = warp - 2;                 // 0..7
+    constexpr uint32_t kBias = 0x4B400000u;  // bits of 1.5 * 2^23
+    const int ew = warp - 2;                 // 0..15
     const int quad = warp & 3;               // TMEM lane quadrant this warp may access
-    const int half = ew >> 2;                // column half of the 256-wide tile
+    const int half = ew >> 2;                // column quarter of the 256-wide tile
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    // bias both accumulator buffers once (completion #0 of tempty[0] and tempty[1])
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int cc = 0; cc < EPI_COLS / 32; ++cc)
+        RRS_TMEM_ST32_SPLAT(tmem_base + lane_off + b * BN + half * EPI_COLS + cc * 32, kBias);
+    ptx::tmem_st_wait();
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      ptx::mbar_arrive(&tempty[0]);
+      ptx::mbar_arrive(&tempty[1]);
+    }
+    const float2 neg_bias2 = make_float2(-12582912.0f, -12582912.0f);  // -1.5*2^23
     uint32_t acc_iter = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
       const int row = m_blk * BM + row_in_tile;
-      const int col0 = n_blk * BN + half * 128;
+      const int col0 = n_blk * BN + half * EPI_COLS;
       // stage beta for this tile (named barrier among the 256 epilogue threads)
       asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
       if (p.w_scale) {
         const int c = threadIdx.x - 64;
         const int n = n_blk * BN + c;
-        beta_sm[c] = (n < p.N) ? p.w_scale[n] : 0.0f;
+        if (c < BN) beta_sm[c] = (n < p.N) ? p.w_scale[n] : 0.0f;
       }
       asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
 
-      float acc[128];
+      float2 acc2[EPI_COLS / 2];  // acc pairs (columns 2i, 2i+1 of this thread's EPI_COLS)
 #pragma unroll
-      for (int c = 0; c < 128; ++c) acc[c] = 0.0f;
+      for (int c = 0; c < EPI_COLS / 2; ++c) acc2[c] = make_float2(0.0f, 0.0f);
       const int ngroups = kPlain ? 1 : p.G;
       for (int g = 0; g < ngroups; ++g) {
         const uint32_t b = acc_iter & 1;
         ptx::mbar_wait(&tfull[b], (acc_iter >> 1) & 1);
         ptx::tc_fence_after();
         const float s = kPlain ? 1.0f : s_sm[g];
-        const uint32_t tbase = tmem_base + lane_off + b * BN + half * 128;
+        const float2 s2 = make_float2(s, s);
+        const uint32_t tbase = tmem_base + lane_off + b * BN + half * EPI_COLS;
 #pragma unroll
-        for (int cc = 0; cc < 4; ++cc) {
-          uint32_t r[32];
-          RRS_TMEM_LD32(tbase + cc * 32, r);
+        for (int cc = 0; cc < EPI_COLS / 16; ++cc) {
+          uint32_t r[16];
+          RRS_TMEM_LD16(tbase + cc * 16, r);
           ptx::tmem_ld_wait();
-          if (p.P_debug != nullptr && row < p.T) {
+          if (kDebug && row < p.T) {
             const int gg = kPlain ? 0 : g;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              const int n = col0 + cc * 32 + j;
-              if (n < p.N) p.P_debug[((int64_t)gg * p.T + row) * p.N + n] = (int32_t)r[j];
+            for (int j = 0; j < 16; ++j) {
+              const int n = col0 + cc * 16 + j;
+              if (n < p.N) p.P_debug[((int64_t)gg * p.T + row) * p.N + n] = (int32_t)(r[j] - kBias);
             }
           }
-          if (kPlain) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc[cc * 32 + j] = (float)(int32_t)r[j];  // exact: |sum| < 2^24
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              // exact int32 -> f32 for |P| < 2^22: bits(1.5*2^23 + P) - 1.5*2^23
-              const float f = __uint_as_float(r[j] + 0x4B400000u) - 12582912.0f;
-              acc[cc * 32 + j] = fmaf(s, f, acc[cc * 32 + j]);
-            }
+          for (int j = 0; j < 8; ++j) {
+            // exact: (1.5*2^23 + P) - 1.5*2^23 = P for |P| < 2^22; then acc += s_g * P (R14)
+            const float2 f = __fadd2_rn(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])),
+                                        neg_bias2);
+            acc2[cc * 8 + j] = __ffma2_rn(s2, f, acc2[cc * 8 + j]);
           }
         }
+#pragma unroll
+        for (int cc = 0; cc < EPI_COLS / 32; ++cc) RRS_TMEM_ST32_SPLAT(tbase + cc * 32, kBias);  // re-arm
+        ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&tempty[b]);
         ++acc_iter;
+      }
+      float acc[EPI_COLS];
+#pragma unroll
+      for (int c = 0; c < EPI_COLS / 2; ++c) {
+        acc[2 * c] = acc2[c].x;
+        acc[2 * c + 1] = acc2[c].y;
       }
       // ---- epilogue: Y = acc * (alpha_t * out_scale) * beta_n
       if (p.Y != nullptr && row < p.T) {
@@ -210,13 +236,13 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         if constexpr (kF32Out) {
           float* yrow = reinterpret_cast<float*>(p.Y) + (int64_t)row * p.ldy;
 #pragma unroll
-          for (int c = 0; c < 128; c += 4) {
+          for (int c = 0; c < EPI_COLS; c += 4) {
             const int n = col0 + c;
             float4 v;
-            v.x = (acc[c] * rs) * beta_sm[half * 128 + c];
-            v.y = (acc[c + 1] * rs) * beta_sm[half * 128 + c + 1];
-            v.z = (acc[c + 2] * rs) * beta_sm[half * 128 + c + 2];
-            v.w = (acc[c + 3] * rs) * beta_sm[half * 128 + c + 3];
+            v.x = (acc[c] * rs) * beta_sm[half * EPI_COLS + c];
+            v.y = (acc[c + 1] * rs) * beta_sm[half * EPI_COLS + c + 1];
+            v.z = (acc[c + 2] * rs) * beta_sm[half * EPI_COLS + c + 2];
+            v.w = (acc[c + 3] * rs) * beta_sm[half * EPI_COLS + c + 3];
             if (n + 3 < p.N) {
               *reinterpret_cast<float4*>(yrow + n) = v;
             } else {
@@ -228,13 +254,13 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         } else {
           __nv_bfloat16* yrow = reinterpret_cast<__nv_bfloat16*>(p.Y) + (int64_t)row * p.ldy;
 #pragma unroll
-          for (int c = 0; c < 128; c += 8) {
+          for (int c = 0; c < EPI_COLS; c += 8) {
             const int n = col0 + c;
             uint32_t w[4];
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
-              const float a0 = (acc[c + 2 * h] * rs) * beta_sm[half * 128 + c + 2 * h];
-              const float a1 = (acc[c + 2 * h + 1] * rs) * beta_sm[half * 128 + c + 2 * h + 1];
+              const float a0 = (acc[c + 2 * h] * rs) * beta_sm[half * EPI_COLS + c + 2 * h];
+              const float a1 = (acc[c + 2 * h + 1] * rs) * beta_sm[half * EPI_COLS + c + 2 * h + 1];
               const __nv_bfloat162 bb = __floats2bfloat162_rn(a0, a1);
               w[h] = *reinterpret_cast<const uint32_t*>(&bb);
             }
@@ -283,10 +309,10 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t K,
   return r == CUDA_SUCCESS;
 }
 
-template <bool kPlain, bool kF32>
+template <bool kPlain, bool kF32, bool kDebug = false>
 static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, const GemmParams& p, int grid,
                                   cudaStream_t st) {
-  auto kern = rrs_gemm_kernel<kPlain, kF32>;
+  auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM_BYTES);
   if (e != cudaSuccess) return e;
   kern<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(tx, tw, p);
@@ -316,6 +342,7 @@ cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.P_debug = a.P_debug;
   const int grid = std::min(p.num_tiles, nsm);
   const bool f32 = a.y_dtype == 1;
+  if (a.P_debug) return launch_variant<false, true, true>(tx, tw, p, grid, st);
   if (a.plain) return f32 ? launch_variant<true, true>(tx, tw, p, grid, st) : launch_variant<true, false>(tx, tw, p, grid, st);
   return f32 ? launch_variant<false, true>(tx, tw, p, grid, st) : launch_variant<false, false>(tx, tw, p, grid, st);
 }

@@ -1,53 +1,93 @@
 // RRS runtime prologue (rows a1-a6 of SURVEY.md §8) and offline weight preparation (a7), sm_100a.
 //
-//   fwht_colmax_kernel : X~ = X.H (exact, fwht.cuh), c_j = max_t |X~_tj| over all T tokens
-//                        (Eq. 1) via per-thread running maxima + one atomicMax per column per
-//                        CTA on the float bits (valid because |x| >= +0).
-//   fwht_quant_kernel  : recompute X~ (cheaper than an f32 round trip through HBM),
-//                        s_g = max_{j' in g} c[perm[j']] (0 -> 1, R8), Z = X~[perm] * fl(1/s_g)
-//                        (Eq. 2, R9), per-token RTN INT4 (R9-R11), pack (D4) and the
-//                        int8 GEMM operand.  With chan_max == nullptr it is the weight path (a7):
-//                        no smoothing (W is permuted, never scaled).
-//   perm_rank_kernel   : offline reorder helper (R5): perm = argsort(c) descending, ties ascending.
+//   fwht_colmax_kernel  : X~ = X.H (exact, fwht.cuh), written once as f32 [T][K] (L2-resident at the
+//                         prefill shapes), and c_j = max_t |X~_tj| over all T tokens (Eq. 1) via
+//                         per-thread running maxima + one atomicMax per column per CTA on the float bits
+//                         (valid because |x| >= +0).  Rows arrive by TMA bulk copies, double-buffered, so
+//                         the next tile's HBM read overlaps this tile's FP64 butterflies.
+//   smooth_quant_kernel : s_g = max_{j' in g} c[perm[j']] (0 -> 1, R8), Z = X~[perm] * fl(1/s_g)
+//                         (Eq. 2, R9), per-token RTN INT4 (R9-R11), pack (D4) and the int8 GEMM
+//                         operand.  With chan_max == nullptr it is the weight path (a7): no smoothing
+//                         (W is permuted, never scaled).
+//   perm_rank_kernel    : offline reorder helper (R5): perm = argsort(c) descending, ties ascending.
+#include <algorithm>
+
 #include "fwht.cuh"
 #include "kernels.h"
+#include "ptx.cuh"
 
 namespace rrs {
 
+// ------------------------------------------------------------------------------ a1 + a2
+
 template <int K>
-__global__ void __launch_bounds__(FwhtPlan<K>::CTA)
-fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
-                   float* __restrict__ Xr_out) {
+struct ColmaxSmem {
   using P = FwhtPlan<K>;
-  extern __shared__ __align__(16) double sm[];
-  const int tid = threadIdx.x;
+  static constexpr int TILE_D = P::TILE * 8;    // fp64 transpose tile
+  static constexpr int STAGE = P::TILE * 2;     // one bf16 tile
+  static constexpr int BYTES = TILE_D + 2 * STAGE + 64;
+};
+
+template <int K>
+__global__ void __launch_bounds__(FwhtPlan<K>::THREADS)
+fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
+                   float* __restrict__ Xr) {
+  using P = FwhtPlan<K>;
+  using S = ColmaxSmem<K>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  double* sm = reinterpret_cast<double*>(smem);
+  uint16_t* stage = reinterpret_cast<uint16_t*>(smem + S::TILE_D);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::TILE_D + 2 * S::STAGE);
+  const int64_t ntiles = (T + P::R - 1) / P::R;
+
+  auto issue = [&](int64_t tile, int buf) {
+    const int64_t rows = (T - tile * P::R) < P::R ? (T - tile * P::R) : P::R;
+    const uint32_t bytes = (uint32_t)(rows * K * 2);
+    ptx::mbar_arrive_expect_tx(&bar[buf], bytes);
+    ptx::bulk_load(stage + buf * P::TILE, X + tile * P::R * K, bytes, &bar[buf]);
+  };
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
   float cm[P::SLOTS];
 #pragma unroll
-  for (int s = 0; s < P::SLOTS; ++s) cm[s] = 0.0f;
-  for (int64_t r0 = (int64_t)blockIdx.x * P::R; r0 < T; r0 += (int64_t)gridDim.x * P::R) {
-    double v[32];
-    fwht_tile<P>(X, K, T, r0, sm, v);
+  for (int j = 0; j < P::SLOTS; ++j) cm[j] = 0.0f;
+  const bool act = out_active<P>(threadIdx.x);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    ptx::mbar_wait(&bar[buf], (it >> 1) & 1);
+    double v[64];
+    int rr, tp;
+    fwht_tile<P>(stage + buf * P::TILE, sm, v, rr, tp);  // ends with __syncthreads: stage[buf] is free
+    if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
+    const int64_t row = tile * P::R + rr;
+    if (act && row < T) {
+      float* xr = Xr ? Xr + row * K : nullptr;
 #pragma unroll
-    for (int s = 0; s < P::SLOTS; ++s) {
-      int row, col;
-      slot_rc<P>(tid, s, row, col);
-      if (r0 + row < T) {
-        const float f = __double2float_rn(v[s]);
-        cm[s] = fmaxf(cm[s], fabsf(f));
-        if (Xr_out) Xr_out[(r0 + row) * K + col] = f;
+      for (int j = 0; j < P::SLOTS; ++j) {
+        const float f = __double2float_rn(v[j]);
+        cm[j] = fmaxf(cm[j], fabsf(f));
+        if (xr) xr[out_col<P>(tp, j)] = f;
       }
     }
-    __syncthreads();  // next tile's pass A overwrites shared memory
   }
-  if ((int64_t)blockIdx.x * P::R < T) {
+  if (chan_max_bits && act && (int64_t)blockIdx.x < ntiles) {
+    // this thread's columns are the same in every tile (out_col does not depend on the row)
+    const int tp = P::kPow2 ? (int)threadIdx.x % P::TP2 : (int)threadIdx.x;
 #pragma unroll
-    for (int s = 0; s < P::SLOTS; ++s) {
-      int row, col;
-      slot_rc<P>(tid, s, row, col);
-      atomicMax(chan_max_bits + col, __float_as_uint(cm[s]));
-    }
+    for (int j = 0; j < P::SLOTS; ++j) atomicMax(chan_max_bits + out_col<P>(tp, j), __float_as_uint(cm[j]));
   }
 }
+
+// ------------------------------------------------------------------------------ a3 - a6 (and a7)
 
 // max over the `width` consecutive lanes sharing a segment (width = power of two <= 32)
 RRS_DEVICE float seg_max(float m, int width) {
@@ -56,26 +96,51 @@ RRS_DEVICE float seg_max(float m, int width) {
 }
 
 template <int K>
-__global__ void __launch_bounds__(FwhtPlan<K>::CTA)
-fwht_quant_kernel(const uint16_t* __restrict__ X, int64_t T, const int32_t* __restrict__ perm,
-                  const unsigned* __restrict__ chan_max_bits, float* __restrict__ s_group_out,
-                  uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out,
-                  int apply_smooth) {
-  using P = FwhtPlan<K>;
-  constexpr int GT = K / 32;                 // gather threads per row (32 output positions each)
-  constexpr int GACT = P::R * GT;            // active gather threads
-  static_assert(GACT <= P::CTA, "gather layout");
-  extern __shared__ __align__(16) double sm[];
-  float* fs = reinterpret_cast<float*>(sm);  // f32 X~ tile, reuses the double tile
-  float* red = reinterpret_cast<float*>(sm + P::R * K);  // 64 floats of reduction scratch
+struct QuantPlan {
+  static constexpr int TPR = K / 32;                                       // threads per row, 32 codes each
+  static constexpr int R = TPR >= 64 ? 1 : 64 / TPR;                       // rows per CTA tile
+  static constexpr int THREADS = R * TPR;
+  static constexpr int TILE = R * K;                                       // f32 elements per tile
+  static constexpr int BYTES = 2 * TILE * 4 + 64 * 4 + 64;                 // 2 stages + reduction + bars
+  static_assert(THREADS <= 1024 && THREADS % 32 == 0, "quant layout");
+};
+
+template <int K>
+__global__ void __launch_bounds__(QuantPlan<K>::THREADS)
+smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __restrict__ perm,
+                    const unsigned* __restrict__ chan_max_bits, float* __restrict__ s_group_out,
+                    uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out) {
+  using Q = QuantPlan<K>;
+  constexpr int TPR = Q::TPR;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float* stage = reinterpret_cast<float*>(smem);
+  float* red = reinterpret_cast<float*>(smem + 2 * Q::TILE * 4);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * Q::TILE * 4 + 64 * 4);
   const int tid = threadIdx.x;
-  const int grow = tid / GT;                 // row within tile handled in the gather phase
-  const int j0 = (tid % GT) * 32;            // first reordered position j'
-  const bool gact = tid < GACT;
+  const int rr = tid / TPR;                 // tile row of this thread
+  const int j0 = (tid % TPR) * 32;          // first reordered position j'
+  const int64_t ntiles = (T + Q::R - 1) / Q::R;
+  const bool smooth = chan_max_bits != nullptr;
+
+  auto issue = [&](int64_t tile, int buf) {
+    const int64_t rows = (T - tile * Q::R) < Q::R ? (T - tile * Q::R) : Q::R;
+    const uint32_t bytes = (uint32_t)(rows * K * 4);
+    ptx::mbar_arrive_expect_tx(&bar[buf], bytes);
+    ptx::bulk_load(stage + buf * Q::TILE, Xr + tile * Q::R * K, bytes, &bar[buf]);
+  };
+  if (tid == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
 
   int pj[32];
-  float inv_s = 1.0f;
-  if (gact) {
+  {
     const int4* pp = reinterpret_cast<const int4*>(perm + j0);
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -83,57 +148,48 @@ fwht_quant_kernel(const uint16_t* __restrict__ X, int64_t T, const int32_t* __re
       pj[4 * q] = w.x; pj[4 * q + 1] = w.y; pj[4 * q + 2] = w.z; pj[4 * q + 3] = w.w;
     }
   }
-  if (apply_smooth) {
+  float inv_s = 1.0f;
+  if (smooth) {
     // s_g = max_{j' in g} c[perm[j']]  (4 consecutive threads cover one 128-wide group)
     float m = 0.0f;
-    if (gact) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) m = fmaxf(m, __uint_as_float(__ldg(chan_max_bits + pj[k])));
-    }
+    for (int k = 0; k < 32; ++k) m = fmaxf(m, __uint_as_float(__ldg(chan_max_bits + pj[k])));
     m = seg_max(m, 4);
     if (m == 0.0f) m = 1.0f;  // R8: zero group -> scale 1
     inv_s = __frcp_rn(m);     // R9: fl(1/s_g)
-    if (blockIdx.x == 0 && gact && grow == 0 && (j0 & 127) == 0) s_group_out[j0 >> 7] = m;
+    if (blockIdx.x == 0 && rr == 0 && (j0 & 127) == 0 && s_group_out) s_group_out[j0 >> 7] = m;
   }
 
-  for (int64_t r0 = (int64_t)blockIdx.x * P::R; r0 < T; r0 += (int64_t)gridDim.x * P::R) {
-    double v[32];
-    fwht_tile<P>(X, K, T, r0, sm, v);
-    __syncthreads();  // all reads of the double tile done
-#pragma unroll
-    for (int s = 0; s < P::SLOTS; ++s) {
-      int row, col;
-      slot_rc<P>(tid, s, row, col);
-      fs[row * K + col] = __double2float_rn(v[s]);
-    }
-    __syncthreads();
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    ptx::mbar_wait(&bar[buf], (it >> 1) & 1);
+    const float* xs = stage + buf * Q::TILE + rr * K;
     float z[32];
     float m = 0.0f;
-    const int64_t trow = r0 + grow;
-    if (gact) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const float x = fs[grow * K + pj[k]];
-        z[k] = apply_smooth ? __fmul_rn(x, inv_s) : x;
-        m = fmaxf(m, fabsf(z[k]));
-      }
+    for (int k = 0; k < 32; ++k) {
+      const float x = xs[pj[k]];
+      z[k] = smooth ? __fmul_rn(x, inv_s) : x;
+      m = fmaxf(m, fabsf(z[k]));
     }
-    // per-token absmax over the GT threads of this row
-    if constexpr (GT <= 32) {
-      m = seg_max(m, GT);
+    // per-token absmax over the TPR threads of this row
+    if constexpr (TPR <= 32) {
+      m = seg_max(m, TPR);
     } else {
       m = seg_max(m, 32);
       if ((tid & 31) == 0) red[tid >> 5] = m;
       __syncthreads();
-      if (gact) {
-        const int w0 = (grow * GT) >> 5;
-        float mm = 0.0f;
+      const int w0 = (rr * TPR) >> 5;
+      float mm = 0.0f;
 #pragma unroll 4
-        for (int w = 0; w < GT / 32; ++w) mm = fmaxf(mm, red[w0 + w]);
-        m = mm;
-      }
+      for (int w = 0; w < TPR / 32; ++w) mm = fmaxf(mm, red[w0 + w]);
+      m = mm;
     }
-    if (gact && trow < T) {
+    __syncthreads();  // every thread has read stage[buf] (and red): both may be reused
+    if (tid == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
+    const int64_t trow = tile * Q::R + rr;
+    if (trow < T) {
       float alpha = 1.0f, r = 0.0f;
       if (m > 0.0f) {
         alpha = __fdiv_rn(m, 7.0f);  // stored scale alpha_t = fl(m/7)
@@ -158,7 +214,6 @@ fwht_quant_kernel(const uint16_t* __restrict__ X, int64_t T, const int32_t* __re
       }
       if (j0 == 0) scale_out[trow] = alpha;
     }
-    __syncthreads();  // fs / red reused by the next tile
   }
 }
 
@@ -180,41 +235,42 @@ __global__ void perm_rank_kernel(const float* __restrict__ c, int K, int32_t* __
 
 // ------------------------------------------------------------------------------- host launchers
 
+template <class F>
+static int grid_for(F kern, int threads, int smem, int64_t tiles, int nsm) {
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  if (per_sm < 1) per_sm = 1;
+  return (int)std::min<int64_t>(tiles, (int64_t)nsm * per_sm);
+}
+
 template <int K>
 static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, float* Xr, int nsm,
                                    cudaStream_t st) {
   using P = FwhtPlan<K>;
   auto kern = fwht_colmax_kernel<K>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM_BYTES);
+  const int smem = ColmaxSmem<K>::BYTES;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::CTA, P::SMEM_BYTES);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t tiles = (T + P::R - 1) / P::R;
-  const int grid = (int)std::min<int64_t>(tiles, (int64_t)nsm * per_sm);
+  const int grid = grid_for(kern, P::THREADS, smem, (T + P::R - 1) / P::R, nsm);
   if (grid == 0) return cudaSuccess;
-  kern<<<grid, P::CTA, P::SMEM_BYTES, st>>>(X, T, cm, Xr);
+  kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr);
   return cudaGetLastError();
 }
 
 template <int K>
-static cudaError_t launch_quant_k(const uint16_t* X, int64_t T, const int32_t* perm, const unsigned* cm,
+static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* perm, const unsigned* cm,
                                   float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, int nsm,
                                   cudaStream_t st) {
-  using P = FwhtPlan<K>;
-  auto kern = fwht_quant_kernel<K>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P::SMEM_BYTES);
+  using Q = QuantPlan<K>;
+  auto kern = smooth_quant_kernel<K>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::BYTES);
   if (e != cudaSuccess) return e;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, P::CTA, P::SMEM_BYTES);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t tiles = (T + P::R - 1) / P::R;
-  int grid = (int)std::min<int64_t>(tiles, (int64_t)nsm * per_sm);
+  int grid = grid_for(kern, Q::THREADS, Q::BYTES, (T + Q::R - 1) / Q::R, nsm);
   if (grid == 0) {
     if (cm == nullptr || s_group == nullptr) return cudaSuccess;
     grid = 1;  // T == 0: still publish s_group (all ones, R8)
   }
-  kern<<<grid, P::CTA, P::SMEM_BYTES, st>>>(X, T, perm, cm, s_group, Xq, Xq8, scale, cm != nullptr);
+  kern<<<grid, Q::THREADS, Q::BYTES, st>>>(Xr, T, perm, cm, s_group, Xq, Xq8, scale);
   return cudaGetLastError();
 }
 
@@ -239,11 +295,11 @@ cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned
   }
 }
 
-cudaError_t launch_fwht_quant(const uint16_t* X, int64_t T, int64_t K, const int32_t* perm,
-                              const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                              float* scale, int nsm, cudaStream_t st) {
+cudaError_t launch_smooth_quant(const float* Xr, int64_t T, int64_t K, const int32_t* perm,
+                                const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
+                                float* scale, int nsm, cudaStream_t st) {
   switch (K) {
-#define RRS_CASE(k) case k: return launch_quant_k<k>(X, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, nsm, st);
+#define RRS_CASE(k) case k: return launch_quant_k<k>(Xr, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, nsm, st);
     RRS_FOR_EACH_K(RRS_CASE)
 #undef RRS_CASE
     default: return cudaErrorInvalidValue;

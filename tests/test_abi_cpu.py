@@ -51,9 +51,9 @@ def test_host_only_calls_work_without_gpu(lib_path):
     l = rrs.lib()
     assert rrs.rrs_version() == 100
     assert l.rrs_status_str(2) == b"RRS_ERR_UNSUPPORTED_SHAPE"
-    # workspace sizing: chan_max + s_group + x_scale + Xq8, 256-byte aligned
+    # workspace sizing: X~ f32 + chan_max + s_group + x_scale + Xq8, 256-byte aligned
     ws = rrs.rrs_workspace_bytes(2048, 4096, 4096, 128, 1)
-    assert ws == 16384 + 256 + 8192 + 2048 * 4096
+    assert ws == 2048 * 4096 * 4 + 16384 + 256 + 8192 + 2048 * 4096
     assert rrs.rrs_workspace_bytes(4, 4, 100, 128, 1) == 0
 
 
