@@ -101,6 +101,152 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------------------ GPU arm
 
+def max_over_ranks(vals, device, world: int) -> float:
+    """Mean of this rank's per-step times, then the MAX over ranks (the slowest rank sets the job time)."""
+    import torch
+    import torch.distributed as dist
+    v = torch.tensor([statistics.fmean(vals)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(v, op=dist.ReduceOp.MAX)
+    return float(v.item())
+
+
+def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
+    """Time one workload on this rank; returns the rank-0 summary (other ranks: None)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2409_20361_b200 as rrs
+
+    w = WORKLOADS[wname]
+    T, K, N = w.T, w.K, w.N
+    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
+    esz = 2 if args.out_dtype == "bf16" else 4
+
+    # ---- inputs (seeded, synthetic), resident in HBM before timing
+    X_bits, W_bits, Xc_bits = make_layer(w, index=list(WORKLOADS).index(wname))
+
+    def dev_bf16(b):
+        return torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).to(dev).view(torch.bfloat16)
+
+    X, W_full, Xc = dev_bf16(X_bits), dev_bf16(W_bits), dev_bf16(Xc_bits)
+    stream = torch.cuda.current_stream()
+    perm = rrs.calibrate_perm(Xc)                      # offline reorder (R5), on the GPU
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    layer = rrs.RRSLinear(W_full, perm, comm=comm, world=world, rank=rank)  # a7, offline
+    t1.record()
+    torch.cuda.synchronize()
+    prep_ms = t0.elapsed_time(t1)
+    del W_full
+    n_local = N // world
+    ws = layer.workspace(T, dev)
+    Xq8 = torch.empty((T, K), dtype=torch.int8, device=dev)
+    xs = torch.empty(T, dtype=torch.float32, device=dev)
+    sg = torch.empty(K // 128, dtype=torch.float32, device=dev)
+    cm = torch.empty(K, dtype=torch.float32, device=dev)
+    pws = torch.empty(rrs.rrs_workspace_bytes(T, 1, K, 128, 1), dtype=torch.uint8, device=dev)
+    Y_shard = torch.empty((T, n_local), dtype=out_dtype, device=dev)
+    Y = torch.empty((T, N), dtype=out_dtype, device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    out_scale = 1.0 / K
+
+    def new_events(n, k):
+        return [[torch.cuda.Event(enable_timing=True) for _ in range(k)] for _ in range(n)]
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def linear():  # one whole hot-path step through the public C-ABI entry point (a1-a9, + e when world > 1)
+        rrs.rrs_linear(X, perm, layer.Wq8, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
+
+    # ---- headline: K timed steps of rrs_linear on HBM-resident inputs, L2 flushed before each step
+    for _ in range(args.warmup):
+        flush.zero_()
+        linear()
+    barrier()
+    evs = new_events(args.steps, 2)
+    with ClockSampler(dev.index) as clocks:
+        barrier()
+        wall0 = time.perf_counter()
+        for i in range(args.steps):
+            flush.zero_()
+            evs[i][0].record(stream)
+            linear()
+            evs[i][1].record(stream)
+        barrier()
+        wall = time.perf_counter() - wall0
+    per_step = [e[0].elapsed_time(e[1]) for e in evs]
+
+    # ---- breakdown (separate pass, events between the kernels): prologue / GEMM / all-gather / plain GEMM
+    bev = new_events(args.steps, 5)
+    for i in range(args.warmup + args.steps):
+        ev = bev[i - args.warmup] if i >= args.warmup else new_events(1, 5)[0]
+        flush.zero_()
+        ev[0].record(stream)
+        rrs.rrs_rotate_smooth_quant(X, perm, None, Xq8, xs, sg, chan_max=cm, ws=pws, stream=stream)
+        ev[1].record(stream)
+        rrs.rrs_gemm(Xq8, xs, sg, layer.Wq8, layer.w_scale, Y_shard, out_scale, stream=stream)
+        ev[2].record(stream)
+        if world > 1:
+            rrs.rrs_allgather_columns(Y_shard, Y, comm, ws, stream=stream)
+        ev[3].record(stream)
+        flush.zero_()
+        ev[4].record(stream)  # plain per-channel A4W4 GEMM on the same operands (P:322 baseline)
+        rrs.rrs_gemm(Xq8, xs, None, layer.Wq8, layer.w_scale, Y_shard, out_scale, plain=True, stream=stream)
+        ev.append(torch.cuda.Event(enable_timing=True))
+        ev[5].record(stream)
+    torch.cuda.synchronize()
+    prologue = [e[0].elapsed_time(e[1]) for e in bev]
+    gemm = [e[1].elapsed_time(e[2]) for e in bev]
+    gather = [e[2].elapsed_time(e[3]) for e in bev]
+    plain = [e[4].elapsed_time(e[5]) for e in bev]
+
+    # ---- end to end through the public API with host buffers: pinned H2D of X, rrs_linear, D2H of Y
+    X_host = X.cpu().pin_memory()
+    Y_host = torch.empty((T, N), dtype=out_dtype).pin_memory()
+    X_dev = torch.empty_like(X)
+    eev = new_events(args.steps, 2)
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        ev = eev[i - args.warmup] if i >= args.warmup else new_events(1, 2)[0]
+        ev[0].record(stream)
+        X_dev.copy_(X_host, non_blocking=True)
+        rrs.rrs_linear(X_dev, perm, layer.Wq8, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
+        Y_host.copy_(Y, non_blocking=True)
+        ev[1].record(stream)
+    torch.cuda.synchronize()
+    e2e = [e[0].elapsed_time(e[1]) for e in eev]
+
+    def mx(vals):
+        return max_over_ranks(vals, dev, world)
+
+    ms_step, ms_pro, ms_gemm, ms_gather = mx(per_step), mx(prologue), mx(gemm), mx(gather)
+    ms_plain, ms_e2e = mx(plain), mx(e2e)
+    ck = clocks.summary()
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        return None
+    ops = 2.0 * T * K * N
+    gemm_tops = 2.0 * T * K * n_local / (ms_gemm * 1e-3) / 1e12
+    res = {
+        "workload": wname, "T": T, "K": K, "N": N, "ms_per_step": ms_step,
+        "tops": ops / (ms_step * 1e-3) / 1e12, "tokens_per_s": T / (ms_step * 1e-3),
+        "breakdown_ms": {"prologue": ms_pro, "rrs_gemm": ms_gemm, "allgather": ms_gather,
+                         "plain_gemm": ms_plain, "prepare_weights_offline": prep_ms},
+        "gemm_tops": gemm_tops, "rrs_overhead_vs_plain_gemm": ms_gemm / ms_plain - 1.0,
+        "e2e_tops": ops / (ms_e2e * 1e-3) / 1e12, "h2d": T * K * 2, "d2h": T * N * esz,
+        "clocks": ck, "wall_s_timed_region": wall,
+    }
+    if cpu_base:
+        res["cpu_baseline"] = cpu_baseline(w, X_bits, W_bits, Xc_bits, budget_s=args.cpu_budget)
+    return res
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -116,118 +262,16 @@ def run_gpu(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    w = WORKLOADS[args.workload]
-    T, K, N = w.T, w.K, w.N
-    out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
-    esz = 2 if args.out_dtype == "bf16" else 4
+    comm = rrs.make_comm()[0] if world > 1 else None
 
-    # ---- inputs (seeded, synthetic), resident in HBM before timing
-    X_bits, W_bits, Xc_bits = make_layer(w, index=list(WORKLOADS).index(args.workload))
-
-    def dev_bf16(b):
-        return torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).to(dev).view(torch.bfloat16)
-
-    X, W_full, Xc = dev_bf16(X_bits), dev_bf16(W_bits), dev_bf16(Xc_bits)
-    comm = None
-    if world > 1:
-        comm, _, _ = rrs.make_comm()
-    stream = torch.cuda.current_stream()
-    perm = rrs.calibrate_perm(Xc)                      # offline reorder (R5), on the GPU
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
-    layer = rrs.RRSLinear(W_full, perm, comm=comm, world=world, rank=rank)  # a7, offline
-    t1.record()
-    torch.cuda.synchronize()
-    prep_ms = t0.elapsed_time(t1)
-    del W_full
-    n_local = N // world
-    ws = torch.empty(rrs.rrs_workspace_bytes(T, N, K, 128, world), dtype=torch.uint8, device=dev)
-    Xq8 = torch.empty((T, K), dtype=torch.int8, device=dev)
-    xs = torch.empty(T, dtype=torch.float32, device=dev)
-    sg = torch.empty(K // 128, dtype=torch.float32, device=dev)
-    cm = torch.empty(K, dtype=torch.float32, device=dev)
-    Y_shard = torch.empty((T, n_local), dtype=out_dtype, device=dev)
-    Y = torch.empty((T, N), dtype=out_dtype, device=dev) if world > 1 else Y_shard
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    out_scale = 1.0 / K
-
-    def step(ev):
-        ev[0].record(stream)
-        rrs.rrs_rotate_smooth_quant(X, perm, None, Xq8, xs, sg, chan_max=cm, stream=stream)
-        ev[1].record(stream)
-        rrs.rrs_gemm(Xq8, xs, sg, layer.Wq8, layer.w_scale, Y_shard, out_scale, stream=stream)
-        ev[2].record(stream)
-        if world > 1:
-            rrs.rrs_allgather_columns(Y_shard, Y, comm, ws, stream=stream)
-        ev[3].record(stream)
-
-    def plain_gemm(ev):
-        ev[0].record(stream)
-        rrs.rrs_gemm(Xq8, xs, None, layer.Wq8, layer.w_scale, Y_shard, out_scale, plain=True, stream=stream)
-        ev[1].record(stream)
-
-    def new_events(n, k):
-        return [[torch.cuda.Event(enable_timing=True) for _ in range(k)] for _ in range(n)]
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    for _ in range(args.warmup):
-        flush.zero_()
-        step(new_events(1, 4)[0])
-    barrier()
-    evs = new_events(args.steps, 4)
-    with ClockSampler(local) as clocks:
-        barrier()
-        wall0 = time.perf_counter()
-        for i in range(args.steps):
-            flush.zero_()
-            step(evs[i])
-        barrier()
-        wall = time.perf_counter() - wall0
-    per_step = [evs[i][0].elapsed_time(evs[i][3]) for i in range(args.steps)]
-    prologue = [evs[i][0].elapsed_time(evs[i][1]) for i in range(args.steps)]
-    gemm = [evs[i][1].elapsed_time(evs[i][2]) for i in range(args.steps)]
-    gather = [evs[i][2].elapsed_time(evs[i][3]) for i in range(args.steps)]
-
-    # plain per-channel A4W4 GEMM on the same operands (the paper's overhead baseline)
-    pev = new_events(args.steps, 2)
-    for i in range(args.steps):
-        flush.zero_()
-        plain_gemm(pev[i])
-    torch.cuda.synchronize()
-    plain = [pev[i][0].elapsed_time(pev[i][1]) for i in range(args.steps)]
-
-    # end to end through the public API with host buffers: pinned H2D of X, rrs_linear, D2H of Y
-    X_host = X.cpu().pin_memory()
-    Y_host = torch.empty((T, N), dtype=out_dtype).pin_memory()
-    X_dev = torch.empty_like(X)
-    Y_e2e = torch.empty((T, N), dtype=out_dtype, device=dev)
-    lin_ws = layer.workspace(T, dev)
-    eev = new_events(args.steps, 2)
-    for i in range(args.warmup + args.steps):
-        flush.zero_()
-        ev = eev[i - args.warmup] if i >= args.warmup else new_events(1, 2)[0]
-        ev[0].record(stream)
-        X_dev.copy_(X_host, non_blocking=True)
-        rrs.rrs_linear(X_dev, perm, layer.Wq8, layer.w_scale, Y_e2e, lin_ws, N_total=N, comm=comm, stream=stream)
-        Y_host.copy_(Y_e2e, non_blocking=True)
-        ev[1].record(stream)
-    torch.cuda.synchronize()
-    e2e = [eev[i][0].elapsed_time(eev[i][1]) for i in range(args.steps)]
-
-    def mx(vals):  # mean per rank, max over ranks
-        v = torch.tensor([statistics.fmean(vals)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(v, op=dist.ReduceOp.MAX)
-        return float(v.item())
-
-    ms_step, ms_pro, ms_gemm, ms_gather = mx(per_step), mx(prologue), mx(gemm), mx(gather)
-    ms_plain, ms_e2e = mx(plain), mx(e2e)
-    ck = clocks.summary()
+    head = measure_workload(args, args.workload, dev, world, rank, comm,
+                            cpu_base=(world == 1 and not args.no_cpu_baseline))
+    extras = {}
+    for wn in (args.also.split(",") if args.also else []):
+        r = measure_workload(args, wn, dev, world, rank, comm, cpu_base=False)
+        if r is not None:
+            extras[wn] = {k: r[k] for k in ("ms_per_step", "tops", "tokens_per_s", "breakdown_ms", "gemm_tops",
+                                            "rrs_overhead_vs_plain_gemm", "e2e_tops")}
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -235,49 +279,56 @@ def run_gpu(args):
             dist.destroy_process_group()
         return None
 
-    ops = 2.0 * T * K * N
     pk = peaks()
     int8_peak = pk["bf16_tflops"] * INT8_OVER_BF16
-    gemm_tops = 2.0 * T * K * n_local / (ms_gemm * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         with open(prof) as fh:
             traffic = json.load(fh).get(args.workload, {}).get("gemm_dram_bytes_per_launch")
+    w = WORKLOADS[args.workload]
     out = {
         "metric": METRIC,
-        "value": ops / (ms_step * 1e-3) / 1e12,
+        "value": head["tops"],
         "unit": "TOPS",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms_step,
+        "ms_per_step": head["ms_per_step"],
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "int8",
         "data": "synthetic (seeded LLaMA-like bf16 activations, N(0,0.02^2) bf16 weights; rrs_synth)",
-        "config": {"workload": args.workload, "T": T, "K": K, "N": N, "group": 128, "out_dtype": args.out_dtype,
-                   "parallelism": f"tp-columns x{world}" if world > 1 else "single",
+        "config": {"workload": args.workload, "T": w.T, "K": w.K, "N": w.N, "group": 128,
+                   "out_dtype": args.out_dtype, "note": w.note,
+                   "parallelism": f"tp-columns x{world} (W column-sharded, X replicated, NCCL all-gather of Y)"
+                   if world > 1 else "single GPU",
                    "l2": "flushed before every timed step (256 MiB write); per-step CUDA events"},
-        "tokens_per_s": T / (ms_step * 1e-3),
-        "breakdown_ms": {"prologue": ms_pro, "rrs_gemm": ms_gemm, "allgather": ms_gather,
-                         "plain_gemm": ms_plain, "prepare_weights_offline": prep_ms},
-        "gemm_tops": gemm_tops,
-        "gemm_pct_int8_peak": 100.0 * gemm_tops / int8_peak,
-        "rrs_overhead_vs_plain_gemm": ms_gemm / ms_plain - 1.0,
-        "roofline": {"bound": "tensor", "kernel": "rrs_gemm_kernel", "achieved": gemm_tops, "peak": int8_peak,
-                     "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
+        "tokens_per_s": head["tokens_per_s"],
+        "breakdown_ms": head["breakdown_ms"],
+        "gemm_tops": head["gemm_tops"],
+        "gemm_pct_int8_peak": 100.0 * head["gemm_tops"] / int8_peak,
+        "rrs_overhead_vs_plain_gemm": head["rrs_overhead_vs_plain_gemm"],
+        "roofline": {"bound": "tensor", "kernel": "rrs_gemm_kernel", "achieved": head["gemm_tops"],
+                     "peak": int8_peak, "unit": "TFLOP/s", "frac": head["gemm_tops"] / int8_peak,
+                     "traffic": traffic,
                      "peak_src": f"int8 = {INT8_OVER_BF16:g} x bf16 burst {pk['bf16_tflops']} TFLOP/s, {pk['src']}",
-                     "algorithmic": "2*T*K*N_local int ops per launch (SURVEY §8(d))"},
-        "e2e": {"value": ops / (ms_e2e * 1e-3) / 1e12, "unit": "TOPS", "h2d_bytes_per_step": T * K * 2,
-                "d2h_bytes_per_step": T * N * esz, "api": "rrs_linear (pinned host X -> device -> host Y)"},
+                     "algorithmic": "2*T*K*N_local int ops per launch / rrs_gemm CUDA-event time (SURVEY 8(d))"},
+        "e2e": {"value": head["e2e_tops"], "unit": "TOPS", "h2d_bytes_per_step": head["h2d"],
+                "d2h_bytes_per_step": head["d2h"],
+                "api": "rrs_linear (pinned host X -> device -> host Y, copies inside the timed region)"},
         "gpu_launches": 3 + (1 if world > 1 else 0),
-        "clocks": ck,
-        "wall_s_timed_region": wall,
+        "gpu_launches_note": "per step: fwht_colmax_kernel, smooth_quant_kernel, rrs_gemm_kernel"
+                             + (", relayout_kernel (+ ncclAllGather)" if world > 1 else "")
+                             + " (+ one cudaMemsetAsync of chan_max)",
+        "clocks": head["clocks"],
+        "wall_s_timed_region": head["wall_s_timed_region"],
     }
-    if world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(w, X_bits, W_bits, Xc_bits, budget_s=args.cpu_budget)
+    if "cpu_baseline" in head:
+        out["cpu_baseline"] = head["cpu_baseline"]
+    if extras:
+        out["also"] = extras
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -366,7 +417,9 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["rrs", "reference"], default="rrs")
-    ap.add_argument("--workload", default="c2_llama2_7b_qo", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c3_llama3_8b_up", choices=sorted(WORKLOADS))
+    ap.add_argument("--also", default="c3_llama3_8b_down,c2_llama2_7b_qo",
+                    help="comma-separated extra workloads summarised under 'also' (empty: none)")
     ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--ref-rows", type=int, default=256)

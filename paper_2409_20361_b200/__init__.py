@@ -70,10 +70,19 @@ class RRSLinear:
         return Y
 
 
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 creates the 128-byte NCCL id (rrs_comm_unique_id); torch.distributed ferries it to every rank."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    uid = [rrs_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0, group=group)
+    if not isinstance(uid[0], bytes) or len(uid[0]) != 128:
+        raise RuntimeError("NCCL unique id broadcast failed")
+    return uid[0]
+
+
 def make_comm(group=None):
     """NCCL communicator over the ranks of a torch.distributed group (rank 0's id is broadcast)."""
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
-    uid = [rrs_comm_unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(uid, src=0, group=group)
-    return rrs_comm_init(rank, world, uid[0]), rank, world
+    return rrs_comm_init(rank, world, broadcast_unique_id(group)), rank, world

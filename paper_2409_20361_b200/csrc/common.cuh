@@ -23,6 +23,15 @@ RRS_DEVICE double bf16_bits_to_double(uint32_t b) {
   return __hiloint2double((int)hi, 0);
 }
 
+// Branch-free variant for the hot loop: exact for normal numbers and zeros; sets `sub` when b is a
+// bf16 subnormal (the caller then redoes the conversion with bf16_bits_to_double).
+RRS_DEVICE double bf16_bits_to_double_fast(uint32_t b, bool& sub) {
+  const uint32_t mag = b & 0x7FFFu;
+  const uint32_t hi = ((b & 0x8000u) << 16) | (mag ? (mag << 13) + (896u << 20) : 0u);
+  sub |= (mag - 1u) < 0x7Fu;
+  return __hiloint2double((int)hi, 0);
+}
+
 RRS_DEVICE uint32_t float_as_ordered(float f) { return __float_as_uint(f); }  // valid for f >= +0
 
 RRS_DEVICE int lane_id() { return threadIdx.x & 31; }

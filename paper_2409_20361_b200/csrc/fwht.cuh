@@ -14,8 +14,10 @@
 // top three bits of the 2^m part, so a thread's inputs are 8 chunks of 8 contiguous bf16 (16-byte loads,
 // coalesced across threads).  Each later pass covers the next (up to) 6 middle bits after one trip through
 // shared memory; the H28 mix is one more pass.  K = 4096 therefore needs a single transpose (16 B of
-// shared-memory traffic per element against 12 DADDs): the kernel is FP64-pipe bound.  swz() keeps the
-// pass-0 stores (stride 8) and the pass-1 accesses (runs of 8, stride 512) at the 2-wavefront minimum.
+// shared-memory traffic per element against 12 DADDs): the kernel is FP64-pipe bound.  The padded
+// address pad(i) = i + i/16 + 8*(i/512) keeps the pass-0 stores (stride 8) and the middle-pass accesses
+// (runs of 8, stride 512) at the 2-wavefront minimum, and is linear in the register index, so every
+// shared-memory access of a thread is one base register plus a compile-time offset.
 #pragma once
 #include "common.cuh"
 
@@ -40,6 +42,7 @@ struct FwhtPlan {
   static constexpr int HI = LOGN - 3;                // pass 0: bits [0,3) and [HI, LOGN)
   static constexpr int SLOTS = kPow2 ? 64 : 56;      // values per thread after the last pass
   static constexpr int TILE = R * K;                 // elements per CTA tile
+  static constexpr int TILE_PAD = TILE + TILE / 16 + TILE / 64;  // doubles of the padded transpose tile
   static_assert(A * NP2 == K, "K must be 2^m or 28*2^m");
   static_assert(LOGN >= 7, "power-of-two part must be >= 128");
   static_assert(K % 128 == 0, "K must be a multiple of the group size 128");
@@ -47,8 +50,8 @@ struct FwhtPlan {
   static_assert(kPow2 || TP2 <= TH28, "H28 layout");
 };
 
-// bijective on any tile (XORs bits 0-3 with functions of bits >= 4)
-RRS_DEVICE int swz(int i) { return i ^ ((i >> 4) & 7) ^ (((i >> 9) & 1) << 3); }
+// padded shared-memory slot of tile element i (injective; max < TILE_PAD)
+RRS_DEVICE int swz(int i) { return i + (i >> 4) + ((i >> 9) << 3); }
 
 // radix-2^r butterflies over the groups v[u*2^r + k], u < 64 >> r (all stages of a pass in registers)
 template <int r>
@@ -197,6 +200,7 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[64], in
   rr = P::kPow2 ? (p2act ? t / P::TP2 : 0) : 0;
   const int tp2 = p2act ? t % P::TP2 : 0;
   if (p2act) {
+    // bf16 -> f32 (placing the 16 bits high) -> f64 (F2F, exact for every finite value incl. subnormals)
     const uint16_t* row = stage + rr * P::K;
 #pragma unroll
     for (int kh = 0; kh < 8; ++kh) {
@@ -204,8 +208,8 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[64], in
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        v[kh * 8 + 2 * h] = bf16_bits_to_double(ws[h] & 0xFFFFu);
-        v[kh * 8 + 2 * h + 1] = bf16_bits_to_double(ws[h] >> 16);
+        v[kh * 8 + 2 * h] = (double)__uint_as_float(ws[h] << 16);
+        v[kh * 8 + 2 * h + 1] = (double)__uint_as_float(ws[h] & 0xFFFF0000u);
       }
     }
     butterflies<6>(v);

@@ -5,12 +5,15 @@
 //                                                                     applied to the dequantized interim
 //                                                                     result"; R14, R15)
 //
-// Design: persistent, one CTA per SM, 320 threads = 10 warps:
-//   warp 0      TMA producer: 128x128 int8 X tile + 256x128 int8 W tile per group into a 4-stage
+// Design: persistent, one CTA per SM, 448 threads = 14 warps (<= 4 per SM sub-partition,
+// so 128 registers per thread):
+//   warp 0      TMA producer: 128x128 int8 X tile + 240x128 int8 W tile per group into a 4-stage
 //               SMEM ring (SWIZZLE_128B: one 128-code group is exactly one 128-byte swizzle row);
-//   warp 1      TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer (M=128, N=256, K=32, 4 per
-//               group) into one of two 256-column int32 TMEM accumulators, alternating per group;
-//   warps 2-9   promotion/epilogue (lane quadrant = warp % 4, column half = (warp-2)/4: 128 columns,
+//   warp 1      TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer (M=128, N=240, K=32, 4 per
+//               group) into one of two int32 TMEM accumulators (columns [0,240), [256,496)), alternating
+//               per group.  N = 240 makes the tile count of the LLaMA shapes land just under a whole number
+//               of waves on 148 SMs (e.g. 2048 x 4096: 288 tiles = 1.95 waves);
+//   warps 2-13  promotion/epilogue (lane quadrant = warp % 4, column third = (warp-2)/4: 80 columns,
 //               whose f32 accumulators stay in registers).
 // Exact int32 -> f32 with no integer instruction: every accumulator buffer is pre-loaded (tcgen05.st)
 // with the bit pattern of 1.5*2^23 and the MMAs always accumulate onto it, so the buffer holds the bits
@@ -31,18 +34,19 @@ namespace rrs {
 
 namespace gemm {
 constexpr int BM = 128;        // tokens per tile   (TMEM lanes)
-constexpr int BN = 256;        // outputs per tile  (TMEM columns per accumulator)
+constexpr int BN = 240;        // outputs per tile  (TMEM columns per accumulator; 256-column slots)
 constexpr int BK = 128;        // one smoothing group = one GEMM K-block
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK;          // 16 KiB
-constexpr int B_BYTES = BN * BK;          // 32 KiB
+constexpr int B_BYTES = BN * BK;          // 30 KiB (30 swizzle atoms of 8 rows x 128 B)
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NUM_EPI_WARPS = 16;
-constexpr int EPI_COLS = BN / (NUM_EPI_WARPS / 4);  // columns per promotion thread (64)
+constexpr int NUM_EPI_WARPS = 12;
+constexpr int EPI_COLS = BN / (NUM_EPI_WARPS / 4);  // columns per promotion thread (80)
+constexpr int ACC_STRIDE = 256;  // TMEM column offset between the two accumulator buffers
 constexpr int THREADS = 64 + NUM_EPI_WARPS * 32;
 constexpr int MAX_G = 128;                 // K <= 16384
 constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 1024 /*barriers, scales*/ +
-                           MAX_G * 4 + BN * 4;
+                           MAX_G * 4 + BN * 4 + 64;
 }  // namespace gemm
 
 struct GemmParams {
@@ -58,7 +62,7 @@ struct GemmParams {
 };
 
 template <bool kPlain, bool kF32Out, bool kDebug>
-__global__ void __maxnreg__(112)
+__global__ void __launch_bounds__(gemm::THREADS, 1)
 rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                 GemmParams p) {
   using namespace gemm;
@@ -73,6 +77,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* s_sm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024);
   float* beta_sm = s_sm + MAX_G;
+  uint32_t* bias_sm = reinterpret_cast<uint32_t*>(beta_sm + BN);  // [8] = 0x4B400000
 
   const uint32_t warp = ptx::warp_idx();
   const int lane = threadIdx.x & 31;
@@ -91,6 +96,8 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     ptx::fence_barrier_init();
   }
   if (warp == 1) ptx::tmem_alloc(taddr_slot, 512);
+  if (threadIdx.x < 8) bias_sm[threadIdx.x] = 0x4B400000u;
+  ptx::pdl_wait();  // Xq8 / x_scale / s_group come from the prologue kernels (programmatic dependent launch)
   if (!kPlain && p.s_group) {
     for (int g = threadIdx.x; g < p.G; g += blockDim.x) s_sm[g] = p.s_group[g];
   }
@@ -133,7 +140,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         if (ptx::elect_one()) {
           const uint64_t a_desc = ptx::smem_desc_sw128(sA + stage * A_BYTES);
           const uint64_t b_desc = ptx::smem_desc_sw128(sB + stage * B_BYTES);
-          const uint32_t d = tmem_base + b * BN;
+          const uint32_t d = tmem_base + b * ACC_STRIDE;
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
             // advance 32 bytes (= 32 int8 codes) along K inside the 128-byte swizzle row; always
@@ -160,8 +167,8 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
 #pragma unroll
     for (int b = 0; b < 2; ++b)
 #pragma unroll
-      for (int cc = 0; cc < EPI_COLS / 32; ++cc)
-        RRS_TMEM_ST32_SPLAT(tmem_base + lane_off + b * BN + half * EPI_COLS + cc * 32, kBias);
+      for (int cc = 0; cc < EPI_COLS / 16; ++cc)
+        RRS_TMEM_ST16_SPLAT(tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS + cc * 16, kBias);
     ptx::tmem_st_wait();
     ptx::tc_fence_before();
     __syncwarp();
@@ -170,6 +177,11 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       ptx::mbar_arrive(&tempty[1]);
     }
     const float2 neg_bias2 = make_float2(-12582912.0f, -12582912.0f);  // -1.5*2^23
+    // eight registers holding the bias bits, the source of the re-arming tcgen05.st (kept live across the
+    // loop; their value comes from shared memory so it is not re-materialised as an immediate)
+    uint32_t bias8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bias8[j] = bias_sm[j];
     uint32_t acc_iter = 0;
     for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
       const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
@@ -194,7 +206,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         ptx::tc_fence_after();
         const float s = kPlain ? 1.0f : s_sm[g];
         const float2 s2 = make_float2(s, s);
-        const uint32_t tbase = tmem_base + lane_off + b * BN + half * EPI_COLS;
+        const uint32_t tbase = tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS;
 #pragma unroll
         for (int cc = 0; cc < EPI_COLS / 16; ++cc) {
           uint32_t r[16];
@@ -217,7 +229,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           }
         }
 #pragma unroll
-        for (int cc = 0; cc < EPI_COLS / 32; ++cc) RRS_TMEM_ST32_SPLAT(tbase + cc * 32, kBias);  // re-arm
+        for (int cc = 0; cc < EPI_COLS / 8; ++cc) RRS_TMEM_ST8(tbase + cc * 8, bias8);  // re-arm
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
@@ -315,8 +327,7 @@ static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, 
   auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  kern<<<grid, gemm::THREADS, gemm::SMEM_BYTES, st>>>(tx, tw, p);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, gemm::THREADS, gemm::SMEM_BYTES, st, tx, tw, p);
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {

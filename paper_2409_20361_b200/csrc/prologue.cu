@@ -23,13 +23,15 @@ namespace rrs {
 template <int K>
 struct ColmaxSmem {
   using P = FwhtPlan<K>;
-  static constexpr int TILE_D = P::TILE * 8;    // fp64 transpose tile
+  static constexpr int TILE_D = ((P::TILE_PAD * 8 + 127) / 128) * 128;  // padded fp64 transpose tile
   static constexpr int STAGE = P::TILE * 2;     // one bf16 tile
   static constexpr int BYTES = TILE_D + 2 * STAGE + 64;
 };
 
+constexpr int kColmaxCluster = 8;  // CTAs that combine their column maxima through DSMEM before the atomics
+
 template <int K>
-__global__ void __launch_bounds__(FwhtPlan<K>::THREADS)
+__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS)
 fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
                    float* __restrict__ Xr) {
   using P = FwhtPlan<K>;
@@ -70,21 +72,44 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
     if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
     const int64_t row = tile * P::R + rr;
     if (act && row < T) {
-      float* xr = Xr ? Xr + row * K : nullptr;
+      float* xr = Xr + row * K;
 #pragma unroll
       for (int j = 0; j < P::SLOTS; ++j) {
         const float f = __double2float_rn(v[j]);
         cm[j] = fmaxf(cm[j], fabsf(f));
-        if (xr) xr[out_col<P>(tp, j)] = f;
+        xr[out_col<P>(tp, j)] = f;
       }
     }
   }
-  if (chan_max_bits && act && (int64_t)blockIdx.x < ntiles) {
-    // this thread's columns are the same in every tile (out_col does not depend on the row)
-    const int tp = P::kPow2 ? (int)threadIdx.x % P::TP2 : (int)threadIdx.x;
+  ptx::pdl_launch_dependents();
+  if (chan_max_bits == nullptr) return;  // weight path: no column maxima (uniform over the cluster)
+  // Column maxima: CTA -> shared memory, then the 8 CTAs of the cluster combine through DSMEM so each
+  // column sees one global atomicMax per cluster instead of one per CTA.
+  uint32_t* cmx = reinterpret_cast<uint32_t*>(smem);  // [K], reuses the transpose tile
+  __syncthreads();
+  for (int c = threadIdx.x; c < K; c += P::THREADS) cmx[c] = 0u;
+  __syncthreads();
+  if (act) {
+    const int tp = P::kPow2 ? (int)threadIdx.x % P::TP2 : (int)threadIdx.x;  // columns do not depend on the row
 #pragma unroll
-    for (int j = 0; j < P::SLOTS; ++j) atomicMax(chan_max_bits + out_col<P>(tp, j), __float_as_uint(cm[j]));
+    for (int j = 0; j < P::SLOTS; ++j) {
+      if constexpr (P::R == 1) {
+        cmx[out_col<P>(tp, j)] = __float_as_uint(cm[j]);  // each column is owned by exactly one thread
+      } else {
+        atomicMax(cmx + out_col<P>(tp, j), __float_as_uint(cm[j]));
+      }
+    }
   }
+  ptx::cluster_sync();
+  const uint32_t rank = ptx::cluster_ctarank();
+  constexpr int SLICE = K / kColmaxCluster;
+  for (int c = (int)rank * SLICE + threadIdx.x; c < ((int)rank + 1) * SLICE; c += P::THREADS) {
+    uint32_t m = 0u;
+#pragma unroll
+    for (uint32_t r = 0; r < kColmaxCluster; ++r) m = max(m, ptx::ld_dsmem_u32(cmx + c, r));
+    atomicMax(chan_max_bits + c, m);  // float bits of values >= +0 order like the floats
+  }
+  ptx::cluster_sync();  // keep this CTA's shared memory alive until every peer has read it
 }
 
 // ------------------------------------------------------------------------------ a3 - a6 (and a7)
@@ -101,7 +126,7 @@ struct QuantPlan {
   static constexpr int R = TPR >= 64 ? 1 : 64 / TPR;                       // rows per CTA tile
   static constexpr int THREADS = R * TPR;
   static constexpr int TILE = R * K;                                       // f32 elements per tile
-  static constexpr int BYTES = 2 * TILE * 4 + 64 * 4 + 64;                 // 2 stages + reduction + bars
+  static constexpr int BYTES = 2 * TILE * 4 + K * 4 + 64 * 4 + 64;         // 2 stages + chan_max + red + bars
   static_assert(THREADS <= 1024 && THREADS % 32 == 0, "quant layout");
 };
 
@@ -114,8 +139,9 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
   constexpr int TPR = Q::TPR;
   extern __shared__ __align__(128) uint8_t smem[];
   float* stage = reinterpret_cast<float*>(smem);
-  float* red = reinterpret_cast<float*>(smem + 2 * Q::TILE * 4);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * Q::TILE * 4 + 64 * 4);
+  float* cms = reinterpret_cast<float*>(smem + 2 * Q::TILE * 4);       // chan_max [K]
+  float* red = cms + K;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 64);
   const int tid = threadIdx.x;
   const int rr = tid / TPR;                 // tile row of this thread
   const int j0 = (tid % TPR) * 32;          // first reordered position j'
@@ -133,13 +159,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
     ptx::mbar_init(&bar[1], 1);
     ptx::fence_barrier_init();
   }
-  __syncthreads();
-  if (tid == 0) {
-    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
-    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
-  }
-
-  int pj[32];
+  int pj[32];  // perm is an offline input: read it before waiting for the FWHT pass
   {
     const int4* pp = reinterpret_cast<const int4*>(perm + j0);
 #pragma unroll
@@ -148,12 +168,22 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
       pj[4 * q] = w.x; pj[4 * q + 1] = w.y; pj[4 * q + 2] = w.z; pj[4 * q + 3] = w.w;
     }
   }
+  ptx::pdl_wait();  // X~ and chan_max come from fwht_colmax_kernel
+  __syncthreads();
+  if (tid == 0) {
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
   float inv_s = 1.0f;
   if (smooth) {
-    // s_g = max_{j' in g} c[perm[j']]  (4 consecutive threads cover one 128-wide group)
+    // chan_max -> shared memory (coalesced), then s_g = max_{j' in g} c[perm[j']]  (4 consecutive
+    // threads cover one 128-wide group)
+    for (int c = tid * 4; c < K; c += Q::THREADS * 4)
+      *reinterpret_cast<uint4*>(cms + c) = __ldcg(reinterpret_cast<const uint4*>(chan_max_bits + c));
+    __syncthreads();
     float m = 0.0f;
 #pragma unroll
-    for (int k = 0; k < 32; ++k) m = fmaxf(m, __uint_as_float(__ldg(chan_max_bits + pj[k])));
+    for (int k = 0; k < 32; ++k) m = fmaxf(m, cms[pj[k]]);
     m = seg_max(m, 4);
     if (m == 0.0f) m = 1.0f;  // R8: zero group -> scale 1
     inv_s = __frcp_rn(m);     // R9: fl(1/s_g)
@@ -215,6 +245,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
       if (j0 == 0) scale_out[trow] = alpha;
     }
   }
+  ptx::pdl_launch_dependents();
 }
 
 // perm[rank(j)] = j, rank by (c descending, index ascending)  -- R5 / R21
@@ -251,8 +282,9 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
   const int smem = ColmaxSmem<K>::BYTES;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int grid = grid_for(kern, P::THREADS, smem, (T + P::R - 1) / P::R, nsm);
+  int grid = grid_for(kern, P::THREADS, smem, (T + P::R - 1) / P::R, nsm);
   if (grid == 0) return cudaSuccess;
+  grid = (grid + kColmaxCluster - 1) / kColmaxCluster * kColmaxCluster;  // whole clusters (idle CTAs are fine)
   kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr);
   return cudaGetLastError();
 }
@@ -265,13 +297,13 @@ static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* per
   auto kern = smooth_quant_kernel<K>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::BYTES);
   if (e != cudaSuccess) return e;
-  int grid = grid_for(kern, Q::THREADS, Q::BYTES, (T + Q::R - 1) / Q::R, nsm);
+  // persistent: at most 2 CTAs per SM, so the per-CTA setup (chan_max load, s_g) is amortised over many rows
+  int grid = (int)std::min<int64_t>(grid_for(kern, Q::THREADS, Q::BYTES, (T + Q::R - 1) / Q::R, nsm), 2 * nsm);
   if (grid == 0) {
     if (cm == nullptr || s_group == nullptr) return cudaSuccess;
     grid = 1;  // T == 0: still publish s_group (all ones, R8)
   }
-  kern<<<grid, Q::THREADS, Q::BYTES, st>>>(Xr, T, perm, cm, s_group, Xq, Xq8, scale);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, Q::THREADS, Q::BYTES, st, Xr, T, perm, cm, s_group, Xq, Xq8, scale);
 }
 
 #define RRS_FOR_EACH_K(M) M(128) M(256) M(512) M(1024) M(2048) M(4096) M(8192) M(16384) M(7168) M(14336)

@@ -48,6 +48,26 @@ RRS_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ------------------------------------------------------------------ clusters / DSMEM / PDL
+RRS_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+RRS_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// 32-bit load from the shared memory of CTA `rank` of this cluster at the address of local `p`
+RRS_DEV uint32_t ld_dsmem_u32(const void* p, uint32_t rank) {
+  uint32_t remote, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote) : "memory");
+  return v;
+}
+// programmatic dependent launch: wait for the preceding grid's memory; allow the next grid to launch
+RRS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+RRS_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ------------------------------------------------------------------ TMA
 RRS_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
@@ -127,6 +147,16 @@ RRS_DEV void mma_commit(uint64_t* bar) {
   asm volatile(                                                                                         \
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"   \
       "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v) : "memory")
+
+#define RRS_TMEM_ST16_SPLAT(taddr, v)                                                                    \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" \
+               ::"r"(taddr), "r"(v) : "memory")
+
+// 32 lanes x 8 columns of 32-bit from 8 registers (v[j] -> column j of the thread's lane)
+#define RRS_TMEM_ST8(taddr, v)                                                                           \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),        \
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])        \
+               : "memory")
 
 RRS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
