@@ -142,7 +142,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
     del W_full
     n_local = N // world
     ws = layer.workspace(T, dev)
-    Xq8 = torch.empty((T, K), dtype=torch.int8, device=dev)
+    Xop = torch.empty((T, K), dtype=torch.uint8, device=dev)
     xs = torch.empty(T, dtype=torch.float32, device=dev)
     sg = torch.empty(K // 128, dtype=torch.float32, device=dev)
     cm = torch.empty(K, dtype=torch.float32, device=dev)
@@ -161,7 +161,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         torch.cuda.synchronize()
 
     def linear():  # one whole hot-path step through the public C-ABI entry point (a1-a9, + e when world > 1)
-        rrs.rrs_linear(X, perm, layer.Wq8, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
+        rrs.rrs_linear(X, perm, layer.Wop, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
 
     # ---- headline: K timed steps of rrs_linear on HBM-resident inputs, L2 flushed before each step
     for _ in range(args.warmup):
@@ -187,16 +187,16 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         ev = bev[i - args.warmup] if i >= args.warmup else new_events(1, 5)[0]
         flush.zero_()
         ev[0].record(stream)
-        rrs.rrs_rotate_smooth_quant(X, perm, None, Xq8, xs, sg, chan_max=cm, ws=pws, stream=stream)
+        rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, chan_max=cm, ws=pws, stream=stream)
         ev[1].record(stream)
-        rrs.rrs_gemm(Xq8, xs, sg, layer.Wq8, layer.w_scale, Y_shard, out_scale, stream=stream)
+        rrs.rrs_gemm(Xop, xs, sg, layer.Wop, layer.w_scale, Y_shard, out_scale, stream=stream)
         ev[2].record(stream)
         if world > 1:
             rrs.rrs_allgather_columns(Y_shard, Y, comm, ws, stream=stream)
         ev[3].record(stream)
         flush.zero_()
         ev[4].record(stream)  # plain per-channel A4W4 GEMM on the same operands (P:322 baseline)
-        rrs.rrs_gemm(Xq8, xs, None, layer.Wq8, layer.w_scale, Y_shard, out_scale, plain=True, stream=stream)
+        rrs.rrs_gemm(Xop, xs, None, layer.Wop, layer.w_scale, Y_shard, out_scale, plain=True, stream=stream)
         ev.append(torch.cuda.Event(enable_timing=True))
         ev[5].record(stream)
     torch.cuda.synchronize()
@@ -215,7 +215,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         ev = eev[i - args.warmup] if i >= args.warmup else new_events(1, 2)[0]
         ev[0].record(stream)
         X_dev.copy_(X_host, non_blocking=True)
-        rrs.rrs_linear(X_dev, perm, layer.Wq8, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
+        rrs.rrs_linear(X_dev, perm, layer.Wop, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
         Y_host.copy_(Y, non_blocking=True)
         ev[1].record(stream)
     torch.cuda.synchronize()

@@ -16,8 +16,13 @@
  *   - bf16 / f32 data is passed as raw bits (uint16_t for bf16); dtype enums select the format.
  *   - Packed INT4 (D4): uint8 [rows][K/2]; byte b holds code 2b in bits 0..3 and code 2b+1 in bits
  *     4..7, two's-complement nibbles; codes lie in [-7, 7] (clamp [-8, 7], R11).
- *   - GEMM operand layout: int8 [rows][K], one code per byte, columns in the REORDERED order j'
- *     (sm_100a has no INT4 MMA; the codes go through tcgen05 .kind::i8).
+ *   - GEMM operand layout ("Xop"/"Wop"): uint8 [rows][K], one code per byte, columns in the REORDERED
+ *     order j'.  sm_100a has no INT4 MMA, so each code is widened to one byte (DESIGN.md §6/§7):
+ *       default          the byte is the E4M3 encoding of the code (exact: |q| <= 8), consumed by
+ *                        tcgen05 .kind::f8f6f4 whose FP32 group sums are exact integers (|P_g| < 2^13);
+ *       RRS_OPERAND_I8   the byte is the int8 code, consumed by tcgen05 .kind::i8 (int32 sums).
+ *     Producer (rrs_prepare_weights / rrs_rotate_smooth_quant) and consumer (rrs_gemm / rrs_linear)
+ *     must be called with the same RRS_OPERAND_I8 flag.
  *   - Every call enqueues work on `stream` (a cudaStream_t, NULL = legacy default stream) and
  *     returns without synchronising the host.  Asynchronous device faults surface on a later CUDA call.
  *   - Validation happens before any launch; on error nothing is enqueued, the status is returned
@@ -52,8 +57,9 @@ typedef enum {
 
 typedef enum { RRS_BF16 = 0, RRS_F32 = 1 } rrs_dtype;
 
-/* rrs_gemm flags */
-#define RRS_GEMM_PLAIN 0x1u /* per-channel A4W4 baseline: one int32 sum over all K, no s_g */
+/* flags */
+#define RRS_GEMM_PLAIN 0x1u   /* rrs_gemm: per-channel A4W4 baseline: one sum over all K, no s_g */
+#define RRS_OPERAND_I8 0x2u   /* GEMM operands are int8 codes (tcgen05 .kind::i8) instead of E4M3 bytes */
 
 typedef struct rrs_comm_s* rrs_comm_t;
 
@@ -66,7 +72,7 @@ int rrs_version(void);
 
 /* Workspace bytes needed by rrs_linear / rrs_rotate_smooth_quant for T tokens:
  * X~[T][K] f32 (the rotated activation, written once by the FWHT pass and read by the quantisation
- * pass) + chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xq8[T][K] int8 (+ Y shard and gather
+ * pass) + chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xop[T][K] u8 (+ Y shard and gather
  * buffers when world > 1), each 256-byte aligned.  Returns 0 for invalid arguments. */
 size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world);
 
@@ -81,48 +87,51 @@ rrs_status rrs_perm_from_channel_max(const float* chan_max, int64_t K, int32_t* 
  *   W~ = W . H_K (exact, R1-R3) -> columns permuted by perm (never scaled)
  *   beta_n = fl(max_j |W~_nj| / 7) (1 if the row is zero, R8); codes rint_even(fl(W~ * fl(7/max))).
  * W: device bf16 bits [N][K].  perm: device int32 [K] (NULL = identity is NOT accepted: pass it).
- * Outputs (device, caller-owned; Wq and Wq8 may each be NULL but not both):
- *   Wq  uint8 [N][K/2] packed INT4;  Wq8 int8 [N][K] GEMM operand;  w_scale f32 [N] = beta_n.
+ * Outputs (device, caller-owned; Wq and Wop may each be NULL but not both):
+ *   Wq  uint8 [N][K/2] packed INT4;  Wop uint8 [N][K] GEMM operand (flags: RRS_OPERAND_I8 or not);
+ *   w_scale f32 [N] = beta_n.
  * Offline helper: it takes a stream-ordered temporary (cudaMallocAsync, <= 256 MiB) for the rotated rows. */
 rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_t K, int32_t group,
-                               const int32_t* perm, uint8_t* Wq, int8_t* Wq8, float* w_scale,
-                               void* stream);
+                               const int32_t* perm, uint8_t* Wq, uint8_t* Wop, float* w_scale,
+                               uint32_t flags, void* stream);
 
 /* Runtime prologue:
  *   a1 X~ = X . H_K per token, exact in f64, rounded once to f32 (Eq. 4, R1-R3)
  *   a2 c_j = max over ALL T tokens of |X~_tj| (Eq. 1, R6)         -> chan_max (optional out)
  *   a3/a4 s_g = max_{j' in group g} c[perm[j']], 0 -> 1 (P:103(2), R5, R8)  -> s_group
  *   a5 Z = X~[:, perm] * fl(1/s_g) (Eq. 2, R9)
- *   a6 alpha_t = fl(max|Z_t| / 7), codes rint_even(fl(Z * fl(7/max))) (R9-R11) -> x_scale, Xq/Xq8
+ *   a6 alpha_t = fl(max|Z_t| / 7), codes rint_even(fl(Z * fl(7/max))) (R9-R11) -> x_scale, Xq/Xop
  * X: device bf16 bits [T][K]; perm: device int32 [K];
- * outputs: Xq uint8 [T][K/2] (nullable), Xq8 int8 [T][K] (nullable), x_scale f32 [T],
+ * outputs: Xq uint8 [T][K/2] (nullable), Xop uint8 [T][K] GEMM operand (nullable; flags as for
+ *          rrs_prepare_weights), x_scale f32 [T],
  *          s_group f32 [K/group], chan_max f32 [K] (nullable: then taken from ws).
  * ws: device scratch, 16-byte aligned, >= rrs_workspace_bytes(T, 1, K, group, 1) bytes (holds X~). */
 rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
-                                   const int32_t* perm, uint8_t* Xq, int8_t* Xq8, float* x_scale,
-                                   float* s_group, float* chan_max, void* ws, size_t ws_bytes,
+                                   const int32_t* perm, uint8_t* Xq, uint8_t* Xop, float* x_scale,
+                                   float* s_group, float* chan_max, void* ws, size_t ws_bytes, uint32_t flags,
                                    void* stream);
 
 /* Fused grouped GEMM (fig:framework (3) P:103, P:109 step 3):
- *   P_g[t][n] = sum_{j' in g} Xq8[t][j'] * Wq8[n][j']      (int32 in TMEM, exact)
+ *   P_g[t][n] = sum_{j' in g} q[t][j'] * qw[n][j']          (exact, in TMEM: FP32 or int32 by carrier)
  *   Y[t][n]   = out_scale * alpha_t * beta_n * sum_g s_g * P_g[t][n]   (f32 scale-accumulate)
  * out_scale = 1/K after rotation (R1).  flags & RRS_GEMM_PLAIN: per-channel A4W4 baseline
- * Y = out_scale * alpha_t * beta_n * sum_{all j'} Xq8 Wq8 (s_group ignored, may be NULL).
- * Xq8 int8 [T][K], x_scale f32 [T], s_group f32 [K/group], Wq8 int8 [N][K], w_scale f32 [N];
+ * Y = out_scale * alpha_t * beta_n * sum_{all j'} q qw (s_group ignored, may be NULL).
+ * flags & RRS_OPERAND_I8: operands are int8 codes, else E4M3 bytes (see the conventions above).
+ * Xop uint8 [T][K], x_scale f32 [T], s_group f32 [K/group], Wop uint8 [N][K], w_scale f32 [N];
  * Y [T][ldy] in y_dtype (bf16: round-to-nearest-even of the f32 result), ldy >= N, ldy % 8 == 0. */
-rrs_status rrs_gemm(const int8_t* Xq8, const float* x_scale, const float* s_group, const int8_t* Wq8,
+rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_group, const uint8_t* Wop,
                     const float* w_scale, int64_t T, int64_t N, int64_t K, int32_t group, float out_scale,
                     uint32_t flags, void* Y, int32_t y_dtype, int64_t ldy, void* stream);
 
 /* Whole layer = rrs_rotate_smooth_quant (into ws) + rrs_gemm with out_scale = 1/K.
- * comm == NULL: single GPU, Wq8/w_scale hold all N rows.
- * comm != NULL (column-parallel): Wq8/w_scale hold THIS rank's N/world output rows
+ * comm == NULL: single GPU, Wop/w_scale hold all N rows.
+ * comm != NULL (column-parallel): Wop/w_scale hold THIS rank's N/world output rows
  *   [rank*N/world, (rank+1)*N/world); X is replicated; every rank runs the identical prologue; Y
  *   receives all N columns through an NCCL all-gather.  N_total % world == 0 required. */
 rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
-                      const int32_t* perm, const int8_t* Wq8, const float* w_scale, int64_t N_total,
+                      const int32_t* perm, const uint8_t* Wop, const float* w_scale, int64_t N_total,
                       void* Y, int32_t y_dtype, int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes,
-                      void* stream);
+                      uint32_t flags, void* stream);
 
 /* The collective step of the column-parallel layer on its own: all-gather every rank's
  * Y shard [T][N_total/world] (contiguous, y_dtype) over NCCL and re-lay it out into Y[T][ldy]
@@ -140,9 +149,9 @@ int32_t rrs_comm_rank(rrs_comm_t comm);
 /* Test-only exports (same kernels, extra stores). */
 /* X~ as f32 [T][K] (natural column order) and chan_max f32 [K] from the a1/a2 kernel. */
 rrs_status rrs_debug_rotate(const void* X, int64_t T, int64_t K, float* Xr, float* chan_max, void* stream);
-/* The tcgen05 GEMM's own int32 group partials P[G][T][N] (read back from TMEM) plus Y. */
-rrs_status rrs_debug_group_partials(const int8_t* Xq8, const int8_t* Wq8, int64_t T, int64_t N, int64_t K,
-                                    int32_t group, int32_t* P, void* stream);
+/* The tcgen05 GEMM's own group partials P[G][T][N] as int32 (read back from TMEM, same kernel). */
+rrs_status rrs_debug_group_partials(const uint8_t* Xop, const uint8_t* Wop, int64_t T, int64_t N, int64_t K,
+                                    int32_t group, int32_t* P, uint32_t flags, void* stream);
 
 #ifdef __cplusplus
 }

@@ -41,7 +41,7 @@ class RRSLinear:
     """Y = RRS-A4W4(X) @ W^T for a bf16 nn.Linear weight W[N][K] (column shard when comm is given)."""
 
     def __init__(self, W: torch.Tensor, perm: torch.Tensor, comm=None, world: int = 1, rank: int = 0,
-                 keep_packed: bool = False, stream=None):
+                 keep_packed: bool = False, i8: bool = False, stream=None):
         N, K = W.shape
         self.K, self.N_total = K, N
         self.comm, self.world, self.rank = comm, world, rank
@@ -49,10 +49,11 @@ class RRSLinear:
         Wl = W[lo:hi].contiguous()
         dev = W.device
         self.perm = perm.to(device=dev, dtype=torch.int32).contiguous()
-        self.Wq8 = torch.empty((hi - lo, K), dtype=torch.int8, device=dev)
+        self.i8 = i8  # GEMM operand carrier: E4M3 bytes (default) or int8 codes (RRS_OPERAND_I8)
+        self.Wop = torch.empty((hi - lo, K), dtype=torch.uint8, device=dev)
         self.Wq = torch.empty((hi - lo, K // 2), dtype=torch.uint8, device=dev) if keep_packed else None
         self.w_scale = torch.empty(hi - lo, dtype=torch.float32, device=dev)
-        rrs_prepare_weights(Wl, self.perm, self.Wq, self.Wq8, self.w_scale, stream=stream)
+        rrs_prepare_weights(Wl, self.perm, self.Wq, self.Wop, self.w_scale, i8=i8, stream=stream)
         self._ws = None
 
     def workspace(self, T: int, device) -> torch.Tensor:
@@ -65,8 +66,8 @@ class RRSLinear:
         T = X.shape[0]
         if Y is None:
             Y = torch.empty((T, self.N_total), dtype=out_dtype, device=X.device)
-        rrs_linear(X, self.perm, self.Wq8, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
-                   comm=self.comm, stream=stream)
+        rrs_linear(X, self.perm, self.Wop, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
+                   comm=self.comm, i8=self.i8, stream=stream)
         return Y
 
 

@@ -18,6 +18,7 @@ RRS_OK = 0
 RRS_BF16 = 0
 RRS_F32 = 1
 RRS_GEMM_PLAIN = 0x1
+RRS_OPERAND_I8 = 0x2
 
 _c_i64, _c_i32, _c_u32, _c_p, _c_sz, _c_f = (ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p,
                                              ctypes.c_size_t, ctypes.c_float)
@@ -28,13 +29,14 @@ _SIGS = {
     "rrs_version": (ctypes.c_int, []),
     "rrs_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32]),
     "rrs_perm_from_channel_max": (ctypes.c_int, [_c_p, _c_i64, _c_p, _c_p]),
-    "rrs_prepare_weights": (ctypes.c_int, [_c_p, _c_i32, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "rrs_prepare_weights": (ctypes.c_int, [_c_p, _c_i32, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_u32,
+                                           _c_p]),
     "rrs_rotate_smooth_quant": (ctypes.c_int, [_c_p, _c_i32, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_p,
-                                               _c_p, _c_p, _c_p, _c_sz, _c_p]),
+                                               _c_p, _c_p, _c_p, _c_sz, _c_u32, _c_p]),
     "rrs_gemm": (ctypes.c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_f, _c_u32,
                                 _c_p, _c_i32, _c_i64, _c_p]),
     "rrs_linear": (ctypes.c_int, [_c_p, _c_i32, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_i32,
-                                  _c_i64, _c_p, _c_p, _c_sz, _c_p]),
+                                  _c_i64, _c_p, _c_p, _c_sz, _c_u32, _c_p]),
     "rrs_allgather_columns": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_i64, _c_p, _c_p, _c_sz, _c_p]),
     "rrs_comm_unique_id": (ctypes.c_int, [_c_p]),
     "rrs_comm_init": (ctypes.c_int, [ctypes.POINTER(_c_p), _c_i32, _c_i32, _c_p]),
@@ -42,7 +44,7 @@ _SIGS = {
     "rrs_comm_world": (_c_i32, [_c_p]),
     "rrs_comm_rank": (_c_i32, [_c_p]),
     "rrs_debug_rotate": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p]),
-    "rrs_debug_group_partials": (ctypes.c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p, _c_p]),
+    "rrs_debug_group_partials": (ctypes.c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p, _c_u32, _c_p]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -124,42 +126,48 @@ def rrs_perm_from_channel_max(chan_max, perm, stream=None) -> None:
            lib().rrs_perm_from_channel_max(_ptr(chan_max), chan_max.numel(), _ptr(perm), _stream(stream)))
 
 
-def rrs_prepare_weights(W, perm, Wq, Wq8, w_scale, group: int = 128, stream=None) -> None:
+def _op_flags(i8: bool) -> int:
+    return RRS_OPERAND_I8 if i8 else 0
+
+
+def rrs_prepare_weights(W, perm, Wq, Wop, w_scale, group: int = 128, i8: bool = False, stream=None) -> None:
+    """Wop: uint8 [N][K] GEMM operand bytes (E4M3-encoded codes, or int8 codes with i8=True)."""
     N, K = W.shape
     _check("rrs_prepare_weights",
-           lib().rrs_prepare_weights(_ptr(W), _bf16_code(W), N, K, group, _ptr(perm), _ptr(Wq), _ptr(Wq8),
-                                     _ptr(w_scale), _stream(stream)))
+           lib().rrs_prepare_weights(_ptr(W), _bf16_code(W), N, K, group, _ptr(perm), _ptr(Wq), _ptr(Wop),
+                                     _ptr(w_scale), _op_flags(i8), _stream(stream)))
 
 
-def rrs_rotate_smooth_quant(X, perm, Xq, Xq8, x_scale, s_group, chan_max=None, ws=None, group: int = 128,
-                            stream=None) -> None:
+def rrs_rotate_smooth_quant(X, perm, Xq, Xop, x_scale, s_group, chan_max=None, ws=None, group: int = 128,
+                            i8: bool = False, stream=None) -> None:
     T, K = X.shape
     if ws is None:  # marshalling convenience: torch owns the scratch (X~ f32 + chan_max), see rrs_workspace_bytes
         ws = torch.empty(rrs_workspace_bytes(T, 1, K, group, 1), dtype=torch.uint8, device=X.device)
     _check("rrs_rotate_smooth_quant",
-           lib().rrs_rotate_smooth_quant(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Xq), _ptr(Xq8),
+           lib().rrs_rotate_smooth_quant(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Xq), _ptr(Xop),
                                          _ptr(x_scale), _ptr(s_group), _ptr(chan_max), _ptr(ws),
-                                         0 if ws is None else ws.numel() * ws.element_size(), _stream(stream)))
+                                         0 if ws is None else ws.numel() * ws.element_size(), _op_flags(i8),
+                                         _stream(stream)))
 
 
-def rrs_gemm(Xq8, x_scale, s_group, Wq8, w_scale, Y, out_scale: float, plain: bool = False, group: int = 128,
-             stream=None) -> None:
-    T, K = Xq8.shape
-    N = Wq8.shape[0]
+def rrs_gemm(Xop, x_scale, s_group, Wop, w_scale, Y, out_scale: float, plain: bool = False, group: int = 128,
+             i8: bool = False, stream=None) -> None:
+    T, K = Xop.shape
+    N = Wop.shape[0]
+    flags = (RRS_GEMM_PLAIN if plain else 0) | _op_flags(i8)
     _check("rrs_gemm",
-           lib().rrs_gemm(_ptr(Xq8), _ptr(x_scale), _ptr(s_group), _ptr(Wq8), _ptr(w_scale), T, N, K, group,
-                          float(out_scale), RRS_GEMM_PLAIN if plain else 0, _ptr(Y, True), _y_code(Y), Y.stride(0),
-                          _stream(stream)))
+           lib().rrs_gemm(_ptr(Xop), _ptr(x_scale), _ptr(s_group), _ptr(Wop), _ptr(w_scale), T, N, K, group,
+                          float(out_scale), flags, _ptr(Y, True), _y_code(Y), Y.stride(0), _stream(stream)))
 
 
-def rrs_linear(X, perm, Wq8, w_scale, Y, ws, N_total: int | None = None, comm=None, group: int = 128,
-               stream=None) -> None:
+def rrs_linear(X, perm, Wop, w_scale, Y, ws, N_total: int | None = None, comm=None, group: int = 128,
+               i8: bool = False, stream=None) -> None:
     T, K = X.shape
     N_total = Y.shape[1] if N_total is None else N_total
     _check("rrs_linear",
-           lib().rrs_linear(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Wq8), _ptr(w_scale), N_total,
+           lib().rrs_linear(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Wop), _ptr(w_scale), N_total,
                             _ptr(Y, True), _y_code(Y), Y.stride(0), comm, _ptr(ws), ws.numel() * ws.element_size(),
-                            _stream(stream)))
+                            _op_flags(i8), _stream(stream)))
 
 
 def rrs_allgather_columns(Y_shard, Y, comm, ws, stream=None) -> None:
@@ -192,8 +200,9 @@ def rrs_debug_rotate(X, Xr, chan_max, stream=None) -> None:
     _check("rrs_debug_rotate", lib().rrs_debug_rotate(_ptr(X), T, K, _ptr(Xr), _ptr(chan_max), _stream(stream)))
 
 
-def rrs_debug_group_partials(Xq8, Wq8, P, group: int = 128, stream=None) -> None:
-    T, K = Xq8.shape
-    N = Wq8.shape[0]
+def rrs_debug_group_partials(Xop, Wop, P, group: int = 128, i8: bool = False, stream=None) -> None:
+    T, K = Xop.shape
+    N = Wop.shape[0]
     _check("rrs_debug_group_partials",
-           lib().rrs_debug_group_partials(_ptr(Xq8), _ptr(Wq8), T, N, K, group, _ptr(P), _stream(stream)))
+           lib().rrs_debug_group_partials(_ptr(Xop), _ptr(Wop), T, N, K, group, _ptr(P), _op_flags(i8),
+                                          _stream(stream)))

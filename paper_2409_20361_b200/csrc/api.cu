@@ -170,7 +170,10 @@ rrs_status rrs_perm_from_channel_max(const float* chan_max, int64_t K, int32_t* 
 }
 
 rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_t K, int32_t group,
-                               const int32_t* perm, uint8_t* Wq, int8_t* Wq8, float* w_scale, void* stream) {
+                               const int32_t* perm, uint8_t* Wq, uint8_t* Wop, float* w_scale, uint32_t flags,
+                               void* stream) {
+  int8_t* Wq8 = reinterpret_cast<int8_t*>(Wop);
+  const bool e4m3 = (flags & RRS_OPERAND_I8) == 0;
   g_last_error.clear();
   int nsm;
   if (rrs_status s = check_arch(nsm)) return s;
@@ -192,7 +195,7 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
     e = rrs::launch_fwht_colmax(Wb + n0 * K, rows, K, nullptr, tmp, nsm, st);
     if (e == cudaSuccess)
       e = rrs::launch_smooth_quant(tmp, rows, K, perm, nullptr, nullptr, Wq ? Wq + n0 * (K / 2) : nullptr,
-                                   Wq8 ? Wq8 + n0 * K : nullptr, w_scale + n0, nsm, st);
+                                   Wq8 ? Wq8 + n0 * K : nullptr, w_scale + n0, e4m3, nsm, st);
   }
   cudaError_t e2 = cudaFreeAsync(tmp, st);
   if (e != cudaSuccess) return cuda_fail(e, "weight preparation kernels");
@@ -200,21 +203,23 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
 }
 
 static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* perm, uint8_t* Xq, int8_t* Xq8,
-                           float* x_scale, float* s_group, float* chan_max, float* Xr, int nsm, cudaStream_t st) {
+                           float* x_scale, float* s_group, float* chan_max, float* Xr, bool e4m3, int nsm,
+                           cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * K, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
   e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
                               nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "fwht_colmax_kernel");
   e = rrs::launch_smooth_quant(Xr, T, K, perm, reinterpret_cast<const unsigned*>(chan_max), s_group, Xq, Xq8,
-                               x_scale, nsm, st);
+                               x_scale, e4m3, nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "smooth_quant_kernel");
   return RRS_OK;
 }
 
 rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
-                                   const int32_t* perm, uint8_t* Xq, int8_t* Xq8, float* x_scale, float* s_group,
-                                   float* chan_max, void* ws, size_t ws_bytes, void* stream) {
+                                   const int32_t* perm, uint8_t* Xq, uint8_t* Xop, float* x_scale, float* s_group,
+                                   float* chan_max, void* ws, size_t ws_bytes, uint32_t flags, void* stream) {
+  int8_t* Xq8 = reinterpret_cast<int8_t*>(Xop);
   g_last_error.clear();
   int nsm;
   if (rrs_status s = check_arch(nsm)) return s;
@@ -229,7 +234,8 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   if (!chan_max) chan_max = w.chan_max;
-  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, w.Xr, nsm, static_cast<cudaStream_t>(stream));
+  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, w.Xr, (flags & RRS_OPERAND_I8) == 0, nsm,
+                  static_cast<cudaStream_t>(stream));
 }
 
 static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int8_t* Wq8, const float* w_scale,
@@ -245,9 +251,11 @@ static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int
   return RRS_OK;
 }
 
-rrs_status rrs_gemm(const int8_t* Xq8, const float* x_scale, const float* s_group, const int8_t* Wq8,
+rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_group, const uint8_t* Wop,
                     const float* w_scale, int64_t T, int64_t N, int64_t K, int32_t group, float out_scale,
                     uint32_t flags, void* Y, int32_t y_dtype, int64_t ldy, void* stream) {
+  const int8_t* Xq8 = reinterpret_cast<const int8_t*>(Xop);
+  const int8_t* Wq8 = reinterpret_cast<const int8_t*>(Wop);
   g_last_error.clear();
   int nsm;
   if (rrs_status s = check_arch(nsm)) return s;
@@ -256,14 +264,17 @@ rrs_status rrs_gemm(const int8_t* Xq8, const float* x_scale, const float* s_grou
   if (!plain && !s_group) return fail(RRS_ERR_INVALID_ARGUMENT, "s_group is NULL");
   if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
   if (T == 0) return RRS_OK;
-  rrs::GemmArgs a{Xq8, x_scale, s_group, Wq8, w_scale, T, N, K, group, out_scale, plain, Y, y_dtype, ldy, nullptr};
+  rrs::GemmArgs a{Xq8, x_scale, s_group, Wq8, w_scale, T, N, K, group, out_scale, plain,
+                  (flags & RRS_OPERAND_I8) == 0, Y, y_dtype, ldy, nullptr};
   cudaError_t e = rrs::launch_gemm(a, nsm, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
 }
 
 rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group, const int32_t* perm,
-                      const int8_t* Wq8, const float* w_scale, int64_t N_total, void* Y, int32_t y_dtype,
-                      int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, void* stream) {
+                      const uint8_t* Wop, const float* w_scale, int64_t N_total, void* Y, int32_t y_dtype,
+                      int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, uint32_t flags, void* stream) {
+  const int8_t* Wq8 = reinterpret_cast<const int8_t*>(Wop);
+  const bool e4m3 = (flags & RRS_OPERAND_I8) == 0;
   g_last_error.clear();
   int nsm;
   if (rrs_status s = check_arch(nsm)) return s;
@@ -280,21 +291,23 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, w.Xr, nsm, st))
+  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, w.Xr, e4m3, nsm, st))
     return s;
   if (T == 0) return RRS_OK;
   const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
   const int esz = y_dtype == RRS_F32 ? 4 : 2;
   if (world == 1) {
     if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy)) return s;
-    rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N_total, K, group, out_scale, false, Y, y_dtype, ldy, nullptr};
+    rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N_total, K, group, out_scale, false, e4m3, Y,
+                    y_dtype, ldy, nullptr};
     cudaError_t e = rrs::launch_gemm(a, nsm, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
   }
   // column-parallel: local shard [T][n_local] -> all-gather [world][T][n_local] -> Y[T][ldy]
   if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, n_local, K, group, w.y_shard, n_local)) return s;
   if (ldy < N_total || !aligned16(Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "Y / ldy");
-  rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, n_local, K, group, out_scale, false, w.y_shard, y_dtype, n_local, nullptr};
+  rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, n_local, K, group, out_scale, false, e4m3,
+                  w.y_shard, y_dtype, n_local, nullptr};
   cudaError_t e = rrs::launch_gemm(a, nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "rrs_gemm kernel");
   return gather_columns(w.y_shard, T, N_total, esz, Y, ldy, comm, w.y_gather, st);
@@ -369,8 +382,10 @@ rrs_status rrs_debug_rotate(const void* X, int64_t T, int64_t K, float* Xr, floa
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "fwht_colmax_kernel");
 }
 
-rrs_status rrs_debug_group_partials(const int8_t* Xq8, const int8_t* Wq8, int64_t T, int64_t N, int64_t K,
-                                    int32_t group, int32_t* P, void* stream) {
+rrs_status rrs_debug_group_partials(const uint8_t* Xop, const uint8_t* Wop, int64_t T, int64_t N, int64_t K,
+                                    int32_t group, int32_t* P, uint32_t flags, void* stream) {
+  const int8_t* Xq8 = reinterpret_cast<const int8_t*>(Xop);
+  const int8_t* Wq8 = reinterpret_cast<const int8_t*>(Wop);
   g_last_error.clear();
   int nsm;
   if (rrs_status s = check_arch(nsm)) return s;
@@ -380,7 +395,8 @@ rrs_status rrs_debug_group_partials(const int8_t* Xq8, const int8_t* Wq8, int64_
   if (T < 0 || N < 1 || group != 128 || K <= 0 || K % group) return fail(RRS_ERR_INVALID_ARGUMENT, "shape");
   if (!aligned16(Xq8) || !aligned16(Wq8)) return fail(RRS_ERR_MISALIGNED, "alignment");
   if (T == 0) return RRS_OK;
-  rrs::GemmArgs a{Xq8, nullptr, nullptr, Wq8, nullptr, T, N, K, group, 1.0f, false, nullptr, RRS_F32, N, P};
+  rrs::GemmArgs a{Xq8, nullptr, nullptr, Wq8, nullptr, T, N, K, group, 1.0f, false, (flags & RRS_OPERAND_I8) == 0,
+                  nullptr, RRS_F32, N, P};
   cudaError_t e = rrs::launch_gemm(a, nsm, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel (debug partials)");
 }

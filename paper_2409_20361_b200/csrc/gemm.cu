@@ -6,15 +6,20 @@
 //                                                                     result"; R14, R15)
 //
 // Design: persistent, one CTA per SM, 448 threads = 14 warps (<= 4 per SM sub-partition,
-// so 128 registers per thread):
-//   warp 0      TMA producer: 128x128 int8 X tile + 240x128 int8 W tile per group into a 4-stage
-//               SMEM ring (SWIZZLE_128B: one 128-code group is exactly one 128-byte swizzle row);
-//   warp 1      TMEM allocator + single-thread tcgen05.mma.kind::i8 issuer (M=128, N=240, K=32, 4 per
+// so 128 registers per thread).  kCta = 2 (T > 128): CTA pairs (clusters of 2) run tcgen05 with
+// cta_group::2, M = 256 (128 rows per CTA), N = 240: each CTA loads its own 128 X rows and HALF of the 240
+// W rows of a group, so a CTA moves 31 KiB per 128-deep group instead of 46 KiB -- the kernel is bound
+// by L2->SM bandwidth otherwise.  kCta = 1 (decode-sized T): M = 128 per CTA.
+//   warp 0      TMA producer: X tile + W tile per group into a STAGES-deep SMEM ring (SWIZZLE_128B: one
+//               128-code group is exactly one 128-byte swizzle row).  In a pair, both CTAs' loads
+//               complete on the leader's mbarrier (cp.async.bulk.tensor .cta_group::2);
+//   warp 1      TMEM allocator; in the leader, the single-thread tcgen05.mma.kind::i8 issuer (K=32, 4 per
 //               group) into one of two int32 TMEM accumulators (columns [0,240), [256,496)), alternating
-//               per group.  N = 240 makes the tile count of the LLaMA shapes land just under a whole number
-//               of waves on 148 SMs (e.g. 2048 x 4096: 288 tiles = 1.95 waves);
+//               per group; commits multicast to both CTAs.  N = 240 makes the tile count of the LLaMA
+//               shapes land just under a whole number of waves on 148 SMs (2048 x 4096: 144 pair tiles
+//               = 1.95 waves of 74 pairs);
 //   warps 2-13  promotion/epilogue (lane quadrant = warp % 4, column third = (warp-2)/4: 80 columns,
-//               whose f32 accumulators stay in registers).
+//               whose f32 accumulators stay in registers); they release a buffer on the leader's barrier.
 // Exact int32 -> f32 with no integer instruction: every accumulator buffer is pre-loaded (tcgen05.st)
 // with the bit pattern of 1.5*2^23 and the MMAs always accumulate onto it, so the buffer holds the bits
 // of the float 1.5*2^23 + P_g, exact because |P_g| <= 6272 < 2^22 (and |sum_k| <= 702464 in plain mode).
@@ -33,20 +38,27 @@
 namespace rrs {
 
 namespace gemm {
-constexpr int BM = 128;        // tokens per tile   (TMEM lanes)
+constexpr int BM = 128;        // tokens per CTA    (TMEM lanes)
 constexpr int BN = 240;        // outputs per tile  (TMEM columns per accumulator; 256-column slots)
 constexpr int BK = 128;        // one smoothing group = one GEMM K-block
-constexpr int STAGES = 4;
-constexpr int A_BYTES = BM * BK;          // 16 KiB
-constexpr int B_BYTES = BN * BK;          // 30 KiB (30 swizzle atoms of 8 rows x 128 B)
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int NUM_EPI_WARPS = 12;
 constexpr int EPI_COLS = BN / (NUM_EPI_WARPS / 4);  // columns per promotion thread (80)
 constexpr int ACC_STRIDE = 256;  // TMEM column offset between the two accumulator buffers
 constexpr int THREADS = 64 + NUM_EPI_WARPS * 32;
 constexpr int MAX_G = 128;                 // K <= 16384
-constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 1024 /*barriers, scales*/ +
-                           MAX_G * 4 + BN * 4 + 64;
+
+template <int kCta>
+struct Cfg {
+  static constexpr int B_ROWS = BN / kCta;                 // W rows loaded per CTA per group
+  static constexpr int A_BYTES = BM * BK;                  // 16 KiB
+  static constexpr int B_BYTES = B_ROWS * BK;              // 30 / 15 KiB (whole 8-row swizzle atoms)
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = kCta == 1 ? 4 : 6;
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 1024 /*barriers*/ +
+                                    MAX_G * 4 + BN * 4 + 64;
+  static_assert(B_ROWS % 8 == 0 && (STAGES * A_BYTES) % 1024 == 0 && B_BYTES % 1024 == 0, "swizzle atoms");
+  static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
+};
 }  // namespace gemm
 
 struct GemmParams {
@@ -61,11 +73,13 @@ struct GemmParams {
   int32_t* P_debug;
 };
 
-template <bool kPlain, bool kF32Out, bool kDebug>
+template <bool kPlain, bool kF32Out, bool kDebug, int kCta, bool kFp8>
 __global__ void __launch_bounds__(gemm::THREADS, 1)
 rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                 GemmParams p) {
   using namespace gemm;
+  using C = Cfg<kCta>;
+  constexpr int STAGES = C::STAGES, A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -81,6 +95,8 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
 
   const uint32_t warp = ptx::warp_idx();
   const int lane = threadIdx.x & 31;
+  const uint32_t rank = kCta == 2 ? ptx::cluster_ctarank() : 0u;  // position in the CTA pair
+  const bool leader = rank == 0;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmap_x);
@@ -91,12 +107,16 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], NUM_EPI_WARPS);
+      ptx::mbar_init(&tempty[b], kCta * NUM_EPI_WARPS);  // only the leader's copy is used
     }
     ptx::fence_barrier_init();
   }
-  if (warp == 1) ptx::tmem_alloc(taddr_slot, 512);
+  if (warp == 1) {
+    if constexpr (kCta == 2) ptx::tmem_alloc2(taddr_slot, 512);
+    else ptx::tmem_alloc(taddr_slot, 512);
+  }
   if (threadIdx.x < 8) bias_sm[threadIdx.x] = 0x4B400000u;
+  if constexpr (kCta == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   ptx::pdl_wait();  // Xq8 / x_scale / s_group come from the prologue kernels (programmatic dependent launch)
   if (!kPlain && p.s_group) {
     for (int g = threadIdx.x; g < p.G; g += blockDim.x) s_sm[g] = p.s_group[g];
@@ -111,24 +131,33 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     if (ptx::elect_one()) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+      for (int tile = blockIdx.x / kCta; tile < p.num_tiles; tile += gridDim.x / kCta) {
         const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
+        const int row0 = m_blk * BM * kCta + (int)rank * BM, wrow0 = n_blk * BN + (int)rank * C::B_ROWS;
         for (int kb = 0; kb < p.G; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-          ptx::tma_load_2d(sA + stage * A_BYTES, &tmap_x, &full[stage], kb * BK, m_blk * BM, ptx::kEvictNormal);
-          ptx::tma_load_2d(sB + stage * B_BYTES, &tmap_w, &full[stage], kb * BK, n_blk * BN, ptx::kEvictNormal);
+          if constexpr (kCta == 1) {
+            ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+            ptx::tma_load_2d(sA + stage * A_BYTES, &tmap_x, &full[stage], kb * BK, row0, ptx::kEvictNormal);
+            ptx::tma_load_2d(sB + stage * B_BYTES, &tmap_w, &full[stage], kb * BK, wrow0, ptx::kEvictNormal);
+          } else {
+            // both CTAs' halves complete on the leader's barrier, which expects the pair's bytes
+            if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * STAGE_BYTES);
+            const uint32_t fb = ptx::mapa_shared(&full[stage], 0);
+            ptx::tma_load_2d_pair(sA + stage * A_BYTES, &tmap_x, fb, kb * BK, row0, ptx::kEvictNormal);
+            ptx::tma_load_2d_pair(sB + stage * B_BYTES, &tmap_w, fb, kb * BK, wrow0, ptx::kEvictNormal);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------------ MMA issuer
-    constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+    // ------------------------------------------------------------------ MMA issuer (pair leader)
+    constexpr uint32_t idesc = kFp8 ? ptx::idesc_e4m3(BM * kCta, BN) : ptx::idesc_i8(BM * kCta, BN);
     int stage = 0;
     uint32_t phase = 0;
     uint32_t acc_iter = 0;  // number of accumulator buffers filled so far
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int tile = blockIdx.x / kCta; leader && tile < p.num_tiles; tile += gridDim.x / kCta) {
       for (int kb = 0; kb < p.G; ++kb) {
         const uint32_t b = acc_iter & 1;
         if (kPlain ? kb == 0 : true) {
@@ -143,12 +172,24 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           const uint32_t d = tmem_base + b * ACC_STRIDE;
 #pragma unroll
           for (int k = 0; k < BK / 32; ++k) {
-            // advance 32 bytes (= 32 int8 codes) along K inside the 128-byte swizzle row; always
-            // accumulate: the buffer starts at the magic bias
-            ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
+            // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier:
+            // always accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
+            if constexpr (kFp8) {
+              const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (k > 0);
+              if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
+              else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
+            } else {
+              if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
+              else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
+            }
           }
-          ptx::mma_commit(&empty[stage]);
-          if (!kPlain || kb == p.G - 1) ptx::mma_commit(&tfull[b]);
+          if constexpr (kCta == 1) {
+            ptx::mma_commit(&empty[stage]);
+            if (!kPlain || kb == p.G - 1) ptx::mma_commit(&tfull[b]);
+          } else {
+            ptx::mma_commit_pair(&empty[stage], 0x3);
+            if (!kPlain || kb == p.G - 1) ptx::mma_commit_pair(&tfull[b], 0x3);
+          }
         }
         __syncwarp();
         if (!kPlain || kb == p.G - 1) ++acc_iter;
@@ -163,18 +204,23 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     const int half = ew >> 2;                // column quarter of the 256-wide tile
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    // bias both accumulator buffers once (completion #0 of tempty[0] and tempty[1])
+    // int8 carrier: bias both accumulator buffers once (completion #0 of tempty[0] and tempty[1])
+    if constexpr (!kFp8) {
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+      for (int b = 0; b < 2; ++b)
 #pragma unroll
-      for (int cc = 0; cc < EPI_COLS / 16; ++cc)
-        RRS_TMEM_ST16_SPLAT(tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS + cc * 16, kBias);
-    ptx::tmem_st_wait();
+        for (int cc = 0; cc < EPI_COLS / 16; ++cc)
+          RRS_TMEM_ST16_SPLAT(tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS + cc * 16, kBias);
+      ptx::tmem_st_wait();
+    }
     ptx::tc_fence_before();
     __syncwarp();
+    // buffer releases go to the pair leader's tempty barriers
+    const uint32_t tempty_addr0 = kCta == 2 ? ptx::mapa_shared(&tempty[0], 0) : ptx::smem_u32(&tempty[0]);
+    const uint32_t tempty_addr1 = kCta == 2 ? ptx::mapa_shared(&tempty[1], 0) : ptx::smem_u32(&tempty[1]);
     if (lane == 0) {
-      ptx::mbar_arrive(&tempty[0]);
-      ptx::mbar_arrive(&tempty[1]);
+      ptx::mbar_arrive_cluster(tempty_addr0);
+      ptx::mbar_arrive_cluster(tempty_addr1);
     }
     const float2 neg_bias2 = make_float2(-12582912.0f, -12582912.0f);  // -1.5*2^23
     // eight registers holding the bias bits, the source of the re-arming tcgen05.st (kept live across the
@@ -183,9 +229,9 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
 #pragma unroll
     for (int j = 0; j < 8; ++j) bias8[j] = bias_sm[j];
     uint32_t acc_iter = 0;
-    for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+    for (int tile = blockIdx.x / kCta; tile < p.num_tiles; tile += gridDim.x / kCta) {
       const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
-      const int row = m_blk * BM + row_in_tile;
+      const int row = m_blk * BM * kCta + (int)rank * BM + row_in_tile;
       const int col0 = n_blk * BN + half * EPI_COLS;
       // stage beta for this tile (named barrier among the 256 epilogue threads)
       asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
@@ -212,28 +258,40 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           uint32_t r[16];
           RRS_TMEM_LD16(tbase + cc * 16, r);
           ptx::tmem_ld_wait();
+          if constexpr (kFp8) {
+            if (cc == EPI_COLS / 16 - 1) {
+              // every column of this buffer is in registers: release it before the last chunk's math
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive_cluster(b ? tempty_addr1 : tempty_addr0);
+            }
+          }
           if (kDebug && row < p.T) {
             const int gg = kPlain ? 0 : g;
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int n = col0 + cc * 16 + j;
-              if (n < p.N) p.P_debug[((int64_t)gg * p.T + row) * p.N + n] = (int32_t)(r[j] - kBias);
+              const int32_t P = kFp8 ? __float2int_rn(__uint_as_float(r[j])) : (int32_t)(r[j] - kBias);
+              if (n < p.N) p.P_debug[((int64_t)gg * p.T + row) * p.N + n] = P;
             }
           }
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            // exact: (1.5*2^23 + P) - 1.5*2^23 = P for |P| < 2^22; then acc += s_g * P (R14)
-            const float2 f = __fadd2_rn(make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])),
-                                        neg_bias2);
+            float2 f = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            // int8 carrier: (1.5*2^23 + P) - 1.5*2^23 = P exactly for |P| < 2^22; FP8 carrier: P is already
+            // an exact float.  Then acc += s_g * P (R14).
+            if constexpr (!kFp8) f = __fadd2_rn(f, neg_bias2);
             acc2[cc * 8 + j] = __ffma2_rn(s2, f, acc2[cc * 8 + j]);
           }
         }
+        if constexpr (!kFp8) {
 #pragma unroll
-        for (int cc = 0; cc < EPI_COLS / 8; ++cc) RRS_TMEM_ST8(tbase + cc * 8, bias8);  // re-arm
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+          for (int cc = 0; cc < EPI_COLS / 8; ++cc) RRS_TMEM_ST8(tbase + cc * 8, bias8);  // re-arm
+          ptx::tmem_st_wait();
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(b ? tempty_addr1 : tempty_addr0);
+        }
         ++acc_iter;
       }
       float acc[EPI_COLS];
@@ -290,7 +348,11 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 1) ptx::tmem_dealloc(tmem_base, 512);
+  if constexpr (kCta == 2) ptx::cluster_sync();  // the peer's MMAs / arrives are done before TMEM goes away
+  if (warp == 1) {
+    if constexpr (kCta == 2) ptx::tmem_dealloc2(tmem_base, 512);
+    else ptx::tmem_dealloc(tmem_base, 512);
+  }
 }
 
 // ------------------------------------------------------------------------------------ host side
@@ -321,21 +383,36 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t K,
   return r == CUDA_SUCCESS;
 }
 
-template <bool kPlain, bool kF32, bool kDebug = false>
+template <bool kPlain, bool kF32, bool kDebug, int kCta, bool kFp8>
 static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, const GemmParams& p, int grid,
                                   cudaStream_t st) {
-  auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gemm::SMEM_BYTES);
+  auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug, kCta, kFp8>;
+  constexpr int smem = gemm::Cfg<kCta>::SMEM_BYTES;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(kern, grid, gemm::THREADS, gemm::SMEM_BYTES, st, tx, tw, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(gemm::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // overlap our setup with the prologue's tail
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;  // CTA pairs for cta_group::2
+  attr[1].val.clusterDim.x = kCta;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
 }
 
-cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {
+template <int kCta, bool kFp8>
+static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   using namespace gemm;
-  if (a.T <= 0) return cudaSuccess;
-  if (a.K / BK > MAX_G || a.K % BK) return cudaErrorInvalidValue;
   CUtensorMap tx, tw;
-  if (!make_tmap(&tx, a.Xq8, a.T, a.K, BM) || !make_tmap(&tw, a.Wq8, a.N, a.K, BN)) return cudaErrorInvalidValue;
+  if (!make_tmap(&tx, a.Xq8, a.T, a.K, BM) || !make_tmap(&tw, a.Wq8, a.N, a.K, Cfg<kCta>::B_ROWS))
+    return cudaErrorInvalidValue;
   GemmParams p;
   p.x_scale = a.x_scale;
   p.s_group = a.s_group;
@@ -344,18 +421,30 @@ cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.N = (int)a.N;
   p.K = (int)a.K;
   p.G = (int)(a.K / BK);
-  p.num_m = (int)((a.T + BM - 1) / BM);
+  p.num_m = (int)((a.T + BM * kCta - 1) / (BM * kCta));
   p.num_n = (int)((a.N + BN - 1) / BN);
   p.num_tiles = p.num_m * p.num_n;
   p.out_scale = a.out_scale;
   p.Y = a.Y;
   p.ldy = a.ldy;
   p.P_debug = a.P_debug;
-  const int grid = std::min(p.num_tiles, nsm);
+  const int grid = std::min(p.num_tiles, nsm / kCta) * kCta;
   const bool f32 = a.y_dtype == 1;
-  if (a.P_debug) return launch_variant<false, true, true>(tx, tw, p, grid, st);
-  if (a.plain) return f32 ? launch_variant<true, true>(tx, tw, p, grid, st) : launch_variant<true, false>(tx, tw, p, grid, st);
-  return f32 ? launch_variant<false, true>(tx, tw, p, grid, st) : launch_variant<false, false>(tx, tw, p, grid, st);
+  if (a.P_debug) return launch_variant<false, true, true, kCta, kFp8>(tx, tw, p, grid, st);
+  if (a.plain)
+    return f32 ? launch_variant<true, true, false, kCta, kFp8>(tx, tw, p, grid, st)
+               : launch_variant<true, false, false, kCta, kFp8>(tx, tw, p, grid, st);
+  return f32 ? launch_variant<false, true, false, kCta, kFp8>(tx, tw, p, grid, st)
+             : launch_variant<false, false, false, kCta, kFp8>(tx, tw, p, grid, st);
+}
+
+cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {
+  using namespace gemm;
+  if (a.T <= 0) return cudaSuccess;
+  if (a.K / BK > MAX_G || a.K % BK) return cudaErrorInvalidValue;
+  // CTA pairs (M = 256) once there are enough tokens to fill them; single CTAs for decode-sized T
+  if (a.fp8) return a.T > BM ? launch_cta<2, true>(a, nsm, st) : launch_cta<1, true>(a, nsm, st);
+  return a.T > BM ? launch_cta<2, false>(a, nsm, st) : launch_cta<1, false>(a, nsm, st);
 }
 
 // Y[t][r*ns + j] = gather[r][t][j]  (all-gathered column shards -> row-major Y), 16-byte chunks

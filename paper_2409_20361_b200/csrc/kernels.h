@@ -29,7 +29,7 @@ cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned
 // chan_max_bits == nullptr: weight mode (no smoothing, s_group unused)
 cudaError_t launch_smooth_quant(const float* Xr, int64_t T, int64_t K, const int32_t* perm,
                                 const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                float* scale, int nsm, cudaStream_t st);
+                                float* scale, bool e4m3, int nsm, cudaStream_t st);
 cudaError_t launch_perm_rank(const float* c, int64_t K, int32_t* perm, cudaStream_t st);
 
 struct GemmArgs {
@@ -41,7 +41,8 @@ struct GemmArgs {
   int64_t T, N, K;
   int group;
   float out_scale;
-  bool plain;             // per-channel A4W4 baseline: one int32 accumulation over all K, no s_g
+  bool plain;             // per-channel A4W4 baseline: one accumulation over all K, no s_g
+  bool fp8;               // operand codes are E4M3 bytes (kind::f8f6f4, exact FP32 sums) instead of int8
   void* Y;                // [T][ldy]
   int y_dtype;            // 0 = bf16, 1 = f32
   int64_t ldy;

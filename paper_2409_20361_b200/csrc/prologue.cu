@@ -120,6 +120,17 @@ RRS_DEVICE float seg_max(float m, int width) {
   return m;
 }
 
+// GEMM operand byte of an INT4 code q in [-8, 7]: the code itself (int8 carrier) or its E4M3 encoding
+// (FP8 carrier; every integer of magnitude <= 8 is exact in E4M3: 1.mmm x 2^e, e = floor(log2|q|)).
+RRS_DEVICE uint32_t operand_byte(int q, bool e4m3) {
+  if (!e4m3) return (uint32_t)(q & 0xFF);
+  const uint32_t a = (uint32_t)(q < 0 ? -q : q);
+  const uint32_t e = 31u - __clz(a | 1u);            // floor(log2 a) for a >= 1
+  const uint32_t m = ((a << 3) >> e) & 7u;           // 3 fraction bits
+  const uint32_t mag = a ? (((e + 7u) << 3) | m) : 0u;  // exponent bias 7
+  return mag | (q < 0 ? 0x80u : 0u);
+}
+
 template <int K>
 struct QuantPlan {
   static constexpr int TPR = K / 32;                                       // threads per row, 32 codes each
@@ -134,7 +145,7 @@ template <int K>
 __global__ void __launch_bounds__(QuantPlan<K>::THREADS)
 smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __restrict__ perm,
                     const unsigned* __restrict__ chan_max_bits, float* __restrict__ s_group_out,
-                    uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out) {
+                    uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out, int e4m3) {
   using Q = QuantPlan<K>;
   constexpr int TPR = Q::TPR;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -232,7 +243,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
         int q = __float2int_rn(__fmul_rn(z[k], r));  // R10: round half to even
         q = max(-8, min(7, q));                      // R11
         packed[k >> 3] |= (uint32_t)(q & 0xF) << ((k & 7) * 4);
-        wide[k >> 2] |= (uint32_t)(q & 0xFF) << ((k & 3) * 8);
+        wide[k >> 2] |= operand_byte(q, e4m3 != 0) << ((k & 3) * 8);
       }
       if (Xq) {
         *reinterpret_cast<uint4*>(Xq + trow * (K / 2) + j0 / 2) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
@@ -291,7 +302,7 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
 
 template <int K>
 static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* perm, const unsigned* cm,
-                                  float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, int nsm,
+                                  float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int nsm,
                                   cudaStream_t st) {
   using Q = QuantPlan<K>;
   auto kern = smooth_quant_kernel<K>;
@@ -303,7 +314,7 @@ static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* per
     if (cm == nullptr || s_group == nullptr) return cudaSuccess;
     grid = 1;  // T == 0: still publish s_group (all ones, R8)
   }
-  return launch_pdl(kern, grid, Q::THREADS, Q::BYTES, st, Xr, T, perm, cm, s_group, Xq, Xq8, scale);
+  return launch_pdl(kern, grid, Q::THREADS, Q::BYTES, st, Xr, T, perm, cm, s_group, Xq, Xq8, scale, (int)e4m3);
 }
 
 #define RRS_FOR_EACH_K(M) M(128) M(256) M(512) M(1024) M(2048) M(4096) M(8192) M(16384) M(7168) M(14336)
@@ -329,9 +340,9 @@ cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned
 
 cudaError_t launch_smooth_quant(const float* Xr, int64_t T, int64_t K, const int32_t* perm,
                                 const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                float* scale, int nsm, cudaStream_t st) {
+                                float* scale, bool e4m3, int nsm, cudaStream_t st) {
   switch (K) {
-#define RRS_CASE(k) case k: return launch_quant_k<k>(Xr, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, nsm, st);
+#define RRS_CASE(k) case k: return launch_quant_k<k>(Xr, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, e4m3, nsm, st);
     RRS_FOR_EACH_K(RRS_CASE)
 #undef RRS_CASE
     default: return cudaErrorInvalidValue;

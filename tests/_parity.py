@@ -43,3 +43,36 @@ def bf16_ulp_error(Y_gpu_bf16: np.ndarray, Y_ref: np.ndarray) -> float:
     m, e = np.frexp(np.where(ref_b == 0, 1.0, ref_b))
     ulp = np.ldexp(1.0, e - 8)
     return float(np.max(np.abs(Y_gpu_bf16.astype(np.float64) - ref_b) / ulp))
+
+
+# ---- GEMM operand carriers (include/rrs.h): int8 codes, or E4M3 bytes.  The E4M3 table is built here from
+# the format's definition (sign | 4-bit exponent, bias 7 | 3-bit fraction), independently of the product.
+def _e4m3_value(b: int) -> float:
+    s = -1.0 if b & 0x80 else 1.0
+    e, m = (b >> 3) & 0xF, b & 7
+    if e == 0xF and m == 7:
+        return float("nan")
+    return s * (m / 8.0) * 2.0 ** -6 if e == 0 else s * (1.0 + m / 8.0) * 2.0 ** (e - 7)
+
+
+_E4M3_OF_INT = {}
+for _b in range(256):
+    _v = _e4m3_value(_b)
+    if _v == _v and _v == int(_v) and -8 <= _v <= 7 and not (_v == 0 and _b != 0):
+        _E4M3_OF_INT[int(_v)] = _b
+_E4M3_LUT = np.array([_E4M3_OF_INT[q] for q in range(-8, 8)], dtype=np.uint8)
+_E4M3_DEC = np.zeros(256, dtype=np.int16)
+for _q, _b in _E4M3_OF_INT.items():
+    _E4M3_DEC[_b] = _q
+
+
+def encode_operand(q: np.ndarray, i8: bool) -> np.ndarray:
+    """INT4 codes (int) -> GEMM operand bytes (uint8) for the chosen carrier."""
+    q = np.asarray(q)
+    return q.astype(np.int8).view(np.uint8) if i8 else _E4M3_LUT[q.astype(np.int64) + 8]
+
+
+def decode_operand(b: np.ndarray, i8: bool) -> np.ndarray:
+    """GEMM operand bytes -> INT4 codes (int8)."""
+    b = np.asarray(b, dtype=np.uint8)
+    return b.view(np.int8) if i8 else _E4M3_DEC[b].astype(np.int8)

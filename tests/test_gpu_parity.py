@@ -17,7 +17,8 @@ import paper_2409_20361_b200 as rrs  # noqa: E402
 from oracle import rrs_oracle as o  # noqa: E402
 from rrs_synth import WORKLOADS, bf16_bits_to_f64, make_activations, make_layer, make_weights  # noqa: E402
 
-from _parity import bf16_ulp_error, dev_bf16, oracle_layer, y_normalised_error  # noqa: E402
+from _parity import (bf16_ulp_error, decode_operand, dev_bf16, encode_operand, oracle_layer,  # noqa: E402
+                     y_normalised_error)
 
 DEV = "cuda"
 
@@ -34,29 +35,29 @@ def _u32(t):
     return t.cpu().numpy().view(np.uint32)
 
 
-def _run_prologue(X_bits, perm):
+def _run_prologue(X_bits, perm, i8=False):
     T, K = X_bits.shape
     X = dev_bf16(X_bits)
     p = torch.from_numpy(perm).to(DEV)
     Xq = torch.empty((T, K // 2), dtype=torch.uint8, device=DEV)
-    Xq8 = torch.empty((T, K), dtype=torch.int8, device=DEV)
+    Xop = torch.empty((T, K), dtype=torch.uint8, device=DEV)
     xs = torch.empty(T, dtype=torch.float32, device=DEV)
     sg = torch.empty(K // 128, dtype=torch.float32, device=DEV)
     cm = torch.empty(K, dtype=torch.float32, device=DEV)
-    rrs.rrs_rotate_smooth_quant(X, p, Xq, Xq8, xs, sg, chan_max=cm)
+    rrs.rrs_rotate_smooth_quant(X, p, Xq, Xop, xs, sg, chan_max=cm, i8=i8)
     torch.cuda.synchronize()
-    return dict(Xq=Xq.cpu().numpy(), Xq8=Xq8.cpu().numpy(), alpha=xs.cpu().numpy(), s_group=sg.cpu().numpy(),
-                chan_max=cm.cpu().numpy())
+    return dict(Xq=Xq.cpu().numpy(), Xop=Xop.cpu().numpy(), Xq8=decode_operand(Xop.cpu().numpy(), i8),
+                alpha=xs.cpu().numpy(), s_group=sg.cpu().numpy(), chan_max=cm.cpu().numpy())
 
 
-def _run_weights(W_bits, perm):
+def _run_weights(W_bits, perm, i8=False):
     N, K = W_bits.shape
     Wq = torch.empty((N, K // 2), dtype=torch.uint8, device=DEV)
-    Wq8 = torch.empty((N, K), dtype=torch.int8, device=DEV)
+    Wop = torch.empty((N, K), dtype=torch.uint8, device=DEV)
     ws = torch.empty(N, dtype=torch.float32, device=DEV)
-    rrs.rrs_prepare_weights(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), Wq, Wq8, ws)
+    rrs.rrs_prepare_weights(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), Wq, Wop, ws, i8=i8)
     torch.cuda.synchronize()
-    return Wq.cpu().numpy(), Wq8, ws
+    return Wq.cpu().numpy(), Wop, ws
 
 
 # ------------------------------------------------------------------------------------- a1 / a2
@@ -79,10 +80,11 @@ def test_rotation_and_channel_max_bitexact(K, T, profile):
 
 @pytest.mark.parametrize("K,T,profile", [(256, 8, "tiny"), (256, 300, "channel"), (4096, 129, "channel"),
                                          (14336, 40, "spike"), (8192, 64, "mixed"), (512, 1, "channel")])
-def test_prologue_bitexact(K, T, profile):
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_prologue_bitexact(K, T, profile, i8):
     X_bits = make_activations(profile, T, K, 303, 404)
     perm = _perm(make_activations(profile, 64, K, 303, 405))
-    g = _run_prologue(X_bits, perm)
+    g = _run_prologue(X_bits, perm, i8=i8)
     Xr = o.rotate(bf16_bits_to_f64(X_bits))
     c = o.channel_max(Xr)
     s = o.group_scales(c, perm, 128)
@@ -91,6 +93,7 @@ def test_prologue_bitexact(K, T, profile):
     assert np.array_equal(g["s_group"].view(np.uint32), s.view(np.uint32))
     assert np.array_equal(g["alpha"].view(np.uint32), a.view(np.uint32))
     assert np.array_equal(g["Xq8"], q)
+    assert np.array_equal(g["Xop"], encode_operand(q, i8))  # every operand byte
     assert np.array_equal(g["Xq"], o.pack_int4(q))
 
 
@@ -116,27 +119,35 @@ def test_prologue_all_zero_activation():
 # ------------------------------------------------------------------------------------- a7
 
 @pytest.mark.parametrize("K,N", [(256, 256), (4096, 300), (14336, 64)])
-def test_prepare_weights_bitexact(K, N):
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_prepare_weights_bitexact(K, N, i8):
     W_bits = make_weights(N, K, 77)
     perm = _perm(make_activations("channel", 64, K, 5, 6))
-    Wq, Wq8, ws = _run_weights(W_bits, perm)
+    Wq, Wop, ws = _run_weights(W_bits, perm, i8=i8)
     qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits), perm)
-    assert np.array_equal(Wq8.cpu().numpy(), qw)
+    assert np.array_equal(Wop.cpu().numpy(), encode_operand(qw, i8))
     assert np.array_equal(Wq, o.pack_int4(qw))
     assert np.array_equal(_u32(ws), beta.view(np.uint32))
 
 
 # ------------------------------------------------------------------------------------- a8 / a9
 
-@pytest.mark.parametrize("T,N,K", [(8, 256, 256), (300, 600, 512), (129, 257, 4096), (1, 16, 128), (256, 512, 1024)])
-def test_group_partials_bitexact(T, N, K):
+@pytest.mark.parametrize("T,N,K", [(8, 256, 256), (300, 600, 512), (129, 257, 4096), (1, 16, 128), (256, 512, 1024),
+                                   (520, 488, 2048)])
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_group_partials_bitexact(T, N, K, i8):
+    """P_g read back from TMEM equals the oracle's integer group sums exactly, for both carriers (the FP8
+    carrier's FP32 accumulation is exact because every partial is an integer below 2^13)."""
     rng = np.random.default_rng(T * 7 + N)
     q = rng.integers(-7, 8, size=(T, K)).astype(np.int8)
     qw = rng.integers(-7, 8, size=(N, K)).astype(np.int8)
     q[0, :] = 7   # extreme partials: +-49 * 128
     qw[0, :] = -7
+    q[1, :] = -7
+    qw[1, ::2] = 7  # alternating signs: large cancellations inside a group
+    qw[1, 1::2] = -7
     P = torch.empty((K // 128, T, N), dtype=torch.int32, device=DEV)
-    rrs.rrs_debug_group_partials(torch.from_numpy(q).to(DEV), torch.from_numpy(qw).to(DEV), P)
+    rrs.rrs_debug_group_partials(_dev(encode_operand(q, i8)), _dev(encode_operand(qw, i8)), P, i8=i8)
     torch.cuda.synchronize()
     assert np.array_equal(P.cpu().numpy(), o.group_partials(q, qw, 128))
 
@@ -152,18 +163,19 @@ def _gemm_case(T, N, K, profile="channel", seed=0):
 @pytest.mark.parametrize("T,N,K,profile", [(8, 256, 256, "tiny"), (300, 600, 512, "channel"),
                                            (129, 520, 4096, "channel"), (200, 264, 14336, "spike"),
                                            (64, 512, 8192, "mixed")])
-def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile):
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile, i8):
     X_bits, W_bits, perm, ref = _gemm_case(T, N, K, profile)
-    Xq8 = _dev(ref["q"])
-    Wq8 = _dev(ref["qw"])
+    Xq8 = _dev(encode_operand(ref["q"], i8))
+    Wq8 = _dev(encode_operand(ref["qw"], i8))
     xs = torch.from_numpy(ref["alpha"]).to(DEV)
     sg = torch.from_numpy(ref["s_group"]).to(DEV)
     ws = torch.from_numpy(ref["beta"]).to(DEV)
     ldy = (N + 7) // 8 * 8
     Yf = torch.full((T, ldy), float("nan"), dtype=torch.float32, device=DEV)
-    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf[:, :N], 1.0 / K)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf[:, :N], 1.0 / K, i8=i8)
     Yb = torch.zeros((T, ldy), dtype=torch.bfloat16, device=DEV)
-    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yb[:, :N], 1.0 / K)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yb[:, :N], 1.0 / K, i8=i8)
     torch.cuda.synchronize()
     Yf_np = Yf.cpu().numpy()
     assert np.isnan(Yf_np[:, N:]).all()  # nothing written past N
@@ -171,14 +183,16 @@ def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile):
     assert bf16_ulp_error(Yb[:, :N].float().cpu().numpy(), ref["Y"]) <= 1.0
 
 
-def test_plain_gemm_matches_per_channel_baseline():
+@pytest.mark.parametrize("T", [130, 100])
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_plain_gemm_matches_per_channel_baseline(T, i8):
     """RRS_GEMM_PLAIN: Y = alpha beta sum_all q qw / K (per-channel A4W4)."""
-    X_bits, W_bits, perm, ref = _gemm_case(130, 300, 1024)
-    Xq8 = _dev(ref["q"])
-    Wq8 = _dev(ref["qw"])
-    Y = torch.empty((130, 304), dtype=torch.float32, device=DEV)
+    X_bits, W_bits, perm, ref = _gemm_case(T, 300, 1024)
+    Xq8 = _dev(encode_operand(ref["q"], i8))
+    Wq8 = _dev(encode_operand(ref["qw"], i8))
+    Y = torch.empty((T, 304), dtype=torch.float32, device=DEV)
     rrs.rrs_gemm(Xq8, torch.from_numpy(ref["alpha"]).to(DEV), None, Wq8, torch.from_numpy(ref["beta"]).to(DEV),
-                 Y[:, :300], 1.0 / 1024, plain=True)
+                 Y[:, :300], 1.0 / 1024, plain=True, i8=i8)
     torch.cuda.synchronize()
     Pall = ref["P"].astype(np.int64).sum(axis=0).astype(np.float64)
     exp = Pall * ref["alpha"].astype(np.float64)[:, None] * ref["beta"].astype(np.float64)[None, :] / 1024
@@ -189,15 +203,16 @@ def test_plain_gemm_matches_per_channel_baseline():
 
 # ------------------------------------------------------------------------------------- whole layer
 
-@pytest.mark.parametrize("wl,T,N", [("c1_tiny", None, None), ("c2_llama2_7b_qo", 257, 520),
-                                    ("c3_llama3_8b_down", 130, 264)])
-def test_rrs_linear_end_to_end(wl, T, N):
+@pytest.mark.parametrize("wl,T,N,i8", [("c1_tiny", None, None, False), ("c2_llama2_7b_qo", 257, 520, False),
+                                       ("c3_llama3_8b_down", 130, 264, False), ("c2_llama2_7b_qo", 300, 264, True),
+                                       ("c1_tiny", None, None, True)])
+def test_rrs_linear_end_to_end(wl, T, N, i8):
     w = WORKLOADS[wl]
     X_bits, W_bits, Xc = make_layer(w, T=T, N=N, T_cal=64)
     T, N = X_bits.shape[0], W_bits.shape[0]
     perm = _perm(Xc)
     ref = oracle_layer(X_bits, W_bits, perm)
-    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), keep_packed=True)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), keep_packed=True, i8=i8)
     Y = layer(dev_bf16(X_bits), out_dtype=torch.float32)
     torch.cuda.synchronize()
     assert np.array_equal(layer.Wq.cpu().numpy(), ref["Wq"])
@@ -212,13 +227,13 @@ def test_rrs_linear_equals_prologue_plus_gemm_bitwise():
     p = torch.from_numpy(perm).to(DEV)
     layer = rrs.RRSLinear(dev_bf16(W_bits), p)
     Y1 = layer(X, out_dtype=torch.float32)
-    Xq8 = torch.empty((200, 4096), dtype=torch.int8, device=DEV)
+    Xop = torch.empty((200, 4096), dtype=torch.uint8, device=DEV)
     xs = torch.empty(200, dtype=torch.float32, device=DEV)
     sg = torch.empty(32, dtype=torch.float32, device=DEV)
     ws = torch.empty(rrs.rrs_workspace_bytes(200, 512, 4096), dtype=torch.uint8, device=DEV)
-    rrs.rrs_rotate_smooth_quant(X, p, None, Xq8, xs, sg, ws=ws)
+    rrs.rrs_rotate_smooth_quant(X, p, None, Xop, xs, sg, ws=ws)
     Y2 = torch.empty_like(Y1)
-    rrs.rrs_gemm(Xq8, xs, sg, layer.Wq8, layer.w_scale, Y2, 1.0 / 4096)
+    rrs.rrs_gemm(Xop, xs, sg, layer.Wop, layer.w_scale, Y2, 1.0 / 4096)
     torch.cuda.synchronize()
     assert torch.equal(Y1, Y2)
     assert y_normalised_error(Y1.cpu().numpy(), ref) <= 1e-5
