@@ -161,8 +161,10 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       for (int kb = 0; kb < p.G; ++kb) {
         const uint32_t b = acc_iter & 1;
         if (kPlain ? kb == 0 : true) {
-          // use u = acc_iter >> 1 of buffer b needs the (u)-th bias store (completion #u of tempty[b])
-          ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
+          // use u = acc_iter >> 1 of buffer b needs the (u)-th release (completion #u of tempty[b]); the
+          // releases come from both CTAs of a pair (cluster-scope acquire)
+          if constexpr (kCta == 2) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
+          else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
         }
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();

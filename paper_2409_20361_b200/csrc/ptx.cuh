@@ -68,6 +68,19 @@ RRS_DEV uint32_t ld_dsmem_u32(const void* p, uint32_t rank) {
 RRS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 RRS_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// wait with cluster-scope acquire: pairs with mbarrier.arrive.release.cluster from a peer CTA
+RRS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x989680u)
+      : "memory");
+}
+
 // ------------------------------------------------------------------ TMA
 RRS_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");

@@ -143,9 +143,10 @@ def test_group_partials_bitexact(T, N, K, i8):
     qw = rng.integers(-7, 8, size=(N, K)).astype(np.int8)
     q[0, :] = 7   # extreme partials: +-49 * 128
     qw[0, :] = -7
-    q[1, :] = -7
-    qw[1, ::2] = 7  # alternating signs: large cancellations inside a group
-    qw[1, 1::2] = -7
+    if T > 1 and N > 1:
+        q[1, :] = -7
+        qw[1, ::2] = 7  # alternating signs: large cancellations inside a group
+        qw[1, 1::2] = -7
     P = torch.empty((K // 128, T, N), dtype=torch.int32, device=DEV)
     rrs.rrs_debug_group_partials(_dev(encode_operand(q, i8)), _dev(encode_operand(qw, i8)), P, i8=i8)
     torch.cuda.synchronize()
