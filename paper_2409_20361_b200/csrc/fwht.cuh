@@ -10,14 +10,16 @@
 // f32 value, bit-identical to the oracle's f32_rne(sum).  The butterfly stages commute, so they may be
 // run in any bit order.
 //
-// Data movement: every thread holds 64 doubles.  Pass 0 covers index bits {0,1,2} and the
-// top three bits of the 2^m part, so a thread's inputs are 8 chunks of 8 contiguous bf16 (16-byte loads,
-// coalesced across threads).  Each later pass covers the next (up to) 6 middle bits after one trip through
-// shared memory; the H28 mix is one more pass.  K = 4096 therefore needs a single transpose (16 B of
-// shared-memory traffic per element against 12 DADDs): the kernel is FP64-pipe bound.  The padded
-// address pad(i) = i + i/16 + 8*(i/512) keeps the pass-0 stores (stride 8) and the middle-pass accesses
-// (runs of 8, stride 512) at the 2-wavefront minimum, and is linear in the register index, so every
-// shared-memory access of a thread is one base register plus a compile-time offset.
+// Data movement: every thread holds E = 2^B doubles (B = 5 for K = 2^m, 6 for 28*2^m).
+// Pass 0 covers index bits {0,1,2} and the top B-3 bits of the 2^m part, so a thread's inputs are E/8 chunks
+// of 8 contiguous bf16 (16-byte loads, coalesced across threads).  Each later pass covers the next (up to)
+// B middle bits after one trip through shared memory; the H28 mix is one more pass.  E = 32 keeps the
+// register footprint low enough for 16 warps per SM (latency hiding) at the price of a second transpose
+// for K = 4096 (32 B of shared-memory traffic per element against 12 DADDs).  The padded
+// address pad(i) = i + i/16 + c1*(i >> s1) + c2*(i >> s2) is strictly increasing (so injective) and, with the
+// per-plan coefficients found by tools/smem_pad_search.py, gives every half-warp 16 distinct 8-byte slots
+// for the pass-0 stores (stride 8), the middle passes and the H28 pass (conflict-free); it is linear in the
+// register index, so every shared-memory access is one base register plus a compile-time offset.
 #pragma once
 #include "common.cuh"
 
@@ -34,32 +36,40 @@ struct FwhtPlan {
   static constexpr int A = kPow2 ? 1 : 28;          // H28 factor
   static constexpr int NP2 = K / A;                  // power-of-two part
   static constexpr int LOGN = ilog2_c(NP2);
-  static constexpr int TP2 = K / 64;                 // threads per row in the 2^m passes (64 values each)
+  static constexpr int B = kPow2 ? 5 : 6;            // bits per pass
+  static constexpr int E = 1 << B;                   // values per thread in the 2^m passes
+  static constexpr int TP2 = K / E;                  // threads per row in the 2^m passes
   static constexpr int TH28 = kPow2 ? 0 : NP2 / 2;   // threads per row in the H28 pass (2 groups of 28)
   static constexpr int TPR = max_c(TP2, TH28);       // threads per row
-  static constexpr int R = kPow2 ? max_c(1, 64 / TP2) : 1;  // rows per CTA tile (>= 2 warps per CTA)
+  static constexpr int R = kPow2 ? max_c(1, 128 / TP2) : 1;  // rows per CTA tile (>= 4 warps per CTA)
   static constexpr int THREADS = ((R * TPR + 31) / 32) * 32;
-  static constexpr int HI = LOGN - 3;                // pass 0: bits [0,3) and [HI, LOGN)
-  static constexpr int SLOTS = kPow2 ? 64 : 56;      // values per thread after the last pass
+  static constexpr int MIN_BLOCKS = kPow2 ? max_c(1, 512 / THREADS) : 1;  // 16 warps/SM -> <= 128 regs
+  static constexpr int HI = LOGN - (B - 3);          // pass 0: bits [0,3) and [HI, LOGN)
+  static constexpr int SLOTS = kPow2 ? E : 56;       // values per thread after the last pass
   static constexpr int TILE = R * K;                 // elements per CTA tile
-  static constexpr int TILE_PAD = TILE + TILE / 16 + TILE / 64;  // doubles of the padded transpose tile
+  // padding coefficients (tools/smem_pad_search.py): 2^m: i + i/16 + 4(i>>7); 28*2^m: + 4(i>>6) + 4(i>>9)
+  static constexpr int PAD_S1 = kPow2 ? 7 : 6, PAD_C1 = 4;
+  static constexpr int PAD_S2 = 9, PAD_C2 = kPow2 ? 0 : 4;
+  static constexpr int TILE_PAD = TILE + TILE / 16 + PAD_C1 * (TILE >> PAD_S1) + PAD_C2 * (TILE >> PAD_S2) + 8;
   static_assert(A * NP2 == K, "K must be 2^m or 28*2^m");
   static_assert(LOGN >= 7, "power-of-two part must be >= 128");
   static_assert(K % 128 == 0, "K must be a multiple of the group size 128");
   static_assert(THREADS <= 1024, "K too large for one CTA");
   static_assert(kPow2 || TP2 <= TH28, "H28 layout");
+  static_assert(!kPow2 || E >= 32, "pow2 plan");
 };
 
-// padded shared-memory slot of tile element i (injective; max < TILE_PAD)
-RRS_DEVICE int swz(int i) { return i + (i >> 4) + ((i >> 9) << 3); }
+// padded shared-memory slot of tile element i (strictly increasing; max < TILE_PAD)
+template <class P>
+RRS_DEVICE int swz(int i) { return i + (i >> 4) + P::PAD_C1 * (i >> P::PAD_S1) + P::PAD_C2 * (i >> P::PAD_S2); }
 
-// radix-2^r butterflies over the groups v[u*2^r + k], u < 64 >> r (all stages of a pass in registers)
-template <int r>
-RRS_DEVICE void butterflies(double (&v)[64]) {
+// radix-2^r butterflies over the groups v[u*2^r + k], u < E >> r (all stages of a pass in registers)
+template <int r, int E>
+RRS_DEVICE void butterflies(double (&v)[E]) {
 #pragma unroll
   for (int h = 1; h < (1 << r); h <<= 1) {
 #pragma unroll
-    for (int u = 0; u < (64 >> r); ++u) {
+    for (int u = 0; u < (E >> r); ++u) {
 #pragma unroll
       for (int k = 0; k < (1 << r); ++k) {
         if ((k & h) == 0) {
@@ -75,7 +85,7 @@ RRS_DEVICE void butterflies(double (&v)[64]) {
 // Row-local index of register j = kh*8 + kl of row-thread tp in pass 0.
 template <class P>
 RRS_DEVICE int p0_index(int tp, int j) {
-  constexpr int per_chunk = P::NP2 / 64;  // threads per 2^m chunk
+  constexpr int per_chunk = P::NP2 / P::E;  // threads per 2^m chunk
   const int a = tp / per_chunk, t = tp % per_chunk;
   return a * P::NP2 + ((j >> 3) << P::HI) + (t << 3) + (j & 7);
 }
@@ -95,8 +105,8 @@ RRS_DEVICE constexpr int chi13(int a) {
   return a == 0 ? 0 : ((a == 1 || a == 3 || a == 4 || a == 9 || a == 10 || a == 12) ? 1 : -1);
 }
 
-template <int OFF>
-RRS_DEVICE void h28_apply(double (&v)[64]) {
+template <int OFF, int E>
+RRS_DEVICE void h28_apply(double (&v)[E]) {
   double u0[14], u1[14], w0[14], w1[14];
 #pragma unroll
   for (int i = 0; i < 14; ++i) {
@@ -132,31 +142,31 @@ RRS_DEVICE int reg_index(int tp, int j) {
     // group u (2 per thread) = column offset bb inside the 2^m chunk; register a = chunk index
     return (j % 28) * P::NP2 + tp + P::TH28 * (j / 28);
   } else {
-    constexpr int r = min_c(6, P::HI - L);
+    constexpr int r = min_c(P::B, P::HI - L);
     return p2_index<P, L, r>(tp, j >> r, j & ((1 << r) - 1));
   }
 }
 
 template <class P, int L>
-RRS_DEVICE void store_layout(double* sm, int rr, int tp, const double (&v)[64]) {
-  constexpr int n = (L == -2) ? 56 : 64;
+RRS_DEVICE void store_layout(double* sm, int rr, int tp, const double (&v)[P::E]) {
+  constexpr int n = (L == -2) ? 56 : P::E;
 #pragma unroll
-  for (int j = 0; j < n; ++j) sm[swz(rr * P::K + reg_index<P, L>(tp, j))] = v[j];
+  for (int j = 0; j < n; ++j) sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))] = v[j];
 }
 
 template <class P, int L>
-RRS_DEVICE void load_layout(const double* sm, int rr, int tp, double (&v)[64]) {
-  constexpr int n = (L == -2) ? 56 : 64;
+RRS_DEVICE void load_layout(const double* sm, int rr, int tp, double (&v)[P::E]) {
+  constexpr int n = (L == -2) ? 56 : P::E;
 #pragma unroll
-  for (int j = 0; j < n; ++j) v[j] = sm[swz(rr * P::K + reg_index<P, L>(tp, j))];
+  for (int j = 0; j < n; ++j) v[j] = sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))];
 }
 
 // The middle passes [b, HI) following a pass with layout PL; finally the H28 pass.  Ends with v in the
 // layout last_layout<P>().  Every thread of the CTA must call it.
 template <class P, int PL, int b>
-RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, double (&v)[64]) {
+RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, double (&v)[P::E]) {
   if constexpr (b < P::HI) {
-    constexpr int r = min_c(6, P::HI - b);
+    constexpr int r = min_c(P::B, P::HI - b);
     if (p2act) store_layout<P, PL>(sm, rr, tp, v);
     __syncthreads();
     if (p2act) {
@@ -183,7 +193,7 @@ __host__ __device__ constexpr int last_layout() {
   int b = 3, last = -1;
   while (b < P::HI) {
     last = b;
-    b += min_c(6, P::HI - b);
+    b += min_c(P::B, P::HI - b);
   }
   return last;
 }
@@ -193,7 +203,7 @@ __host__ __device__ constexpr int last_layout() {
 // out_col<P>(tp, j) of tile row rr (t = rr * TP2 + tp in the 2^m passes; t = tp for H28).
 // active_rows masks rows beyond the matrix (their lanes still run, on whatever the stage holds).
 template <class P>
-RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[64], int& rr, int& tp) {
+RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], int& rr, int& tp) {
   const int t = threadIdx.x;
   const bool p2act = t < P::R * P::TP2;
   const bool h28act = !P::kPow2 && t < P::TH28;
@@ -203,7 +213,7 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[64], in
     // bf16 -> f32 (placing the 16 bits high) -> f64 (F2F, exact for every finite value incl. subnormals)
     const uint16_t* row = stage + rr * P::K;
 #pragma unroll
-    for (int kh = 0; kh < 8; ++kh) {
+    for (int kh = 0; kh < P::E / 8; ++kh) {
       const uint4 w = *reinterpret_cast<const uint4*>(row + p0_index<P>(tp2, kh * 8));
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -212,7 +222,7 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[64], in
         v[kh * 8 + 2 * h + 1] = (double)__uint_as_float(ws[h] & 0xFFFF0000u);
       }
     }
-    butterflies<6>(v);
+    butterflies<P::B>(v);
   }
   fwht_rest<P, -1, 3>(sm, rr, tp2, p2act, h28act, v);
   tp = P::kPow2 ? tp2 : t;

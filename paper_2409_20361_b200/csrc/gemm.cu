@@ -163,7 +163,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         if (kPlain ? kb == 0 : true) {
           // use u = acc_iter >> 1 of buffer b needs the (u)-th release (completion #u of tempty[b]); the
           // releases come from both CTAs of a pair (cluster-scope acquire)
-          if constexpr (kCta == 2) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
+          if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
           else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
         }
         ptx::mbar_wait(&full[stage], phase);
@@ -221,8 +221,13 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     const uint32_t tempty_addr0 = kCta == 2 ? ptx::mapa_shared(&tempty[0], 0) : ptx::smem_u32(&tempty[0]);
     const uint32_t tempty_addr1 = kCta == 2 ? ptx::mapa_shared(&tempty[1], 0) : ptx::smem_u32(&tempty[1]);
     if (lane == 0) {
-      ptx::mbar_arrive_cluster(tempty_addr0);
-      ptx::mbar_arrive_cluster(tempty_addr1);
+      if constexpr (kFp8) {
+        ptx::mbar_arrive_remote(tempty_addr0);
+        ptx::mbar_arrive_remote(tempty_addr1);
+      } else {
+        ptx::mbar_arrive_cluster(tempty_addr0);
+        ptx::mbar_arrive_cluster(tempty_addr1);
+      }
     }
     const float2 neg_bias2 = make_float2(-12582912.0f, -12582912.0f);  // -1.5*2^23
     // eight registers holding the bias bits, the source of the re-arming tcgen05.st (kept live across the
@@ -265,7 +270,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
               // every column of this buffer is in registers: release it before the last chunk's math
               ptx::tc_fence_before();
               __syncwarp();
-              if (lane == 0) ptx::mbar_arrive_cluster(b ? tempty_addr1 : tempty_addr0);
+              if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
             }
           }
           if (kDebug && row < p.T) {

@@ -18,6 +18,21 @@
 
 namespace rrs {
 
+// Optional per-CTA timeline (bench/micro/prologue_trace.cu builds this file with -DRRS_TRACE): thread 0
+// records %globaltimer at fixed points into g_trace[kernel][cta][slot].
+#ifdef RRS_TRACE
+__device__ unsigned long long g_trace[2][1024][16];
+RRS_DEVICE void trace(int k, int slot) {
+  if (threadIdx.x == 0 && blockIdx.x < 1024 && slot < 16) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_trace[k][blockIdx.x][slot] = t;
+  }
+}
+#else
+RRS_DEVICE void trace(int, int) {}
+#endif
+
 // ------------------------------------------------------------------------------ a1 + a2
 
 template <int K>
@@ -31,7 +46,7 @@ struct ColmaxSmem {
 constexpr int kColmaxCluster = 8;  // CTAs that combine their column maxima through DSMEM before the atomics
 
 template <int K>
-__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS)
+__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
 fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
                    float* __restrict__ Xr) {
   using P = FwhtPlan<K>;
@@ -41,6 +56,7 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
   uint16_t* stage = reinterpret_cast<uint16_t*>(smem + S::TILE_D);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::TILE_D + 2 * S::STAGE);
   const int64_t ntiles = (T + P::R - 1) / P::R;
+  trace(0, 0);
 
   auto issue = [&](int64_t tile, int buf) {
     const int64_t rows = (T - tile * P::R) < P::R ? (T - tile * P::R) : P::R;
@@ -66,9 +82,11 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int buf = it & 1;
     ptx::mbar_wait(&bar[buf], (it >> 1) & 1);
-    double v[64];
+    trace(0, 1 + 2 * (it < 5 ? it : 5));
+    double v[P::E];
     int rr, tp;
     fwht_tile<P>(stage + buf * P::TILE, sm, v, rr, tp);  // ends with __syncthreads: stage[buf] is free
+    trace(0, 2 + 2 * (it < 5 ? it : 5));
     if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
     const int64_t row = tile * P::R + rr;
     if (act && row < T) {
@@ -81,6 +99,7 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
       }
     }
   }
+  trace(0, 12);
   ptx::pdl_launch_dependents();
   if (chan_max_bits == nullptr) return;  // weight path: no column maxima (uniform over the cluster)
   // Column maxima: CTA -> shared memory, then the 8 CTAs of the cluster combine through DSMEM so each
@@ -101,6 +120,7 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
     }
   }
   ptx::cluster_sync();
+  trace(0, 13);
   const uint32_t rank = ptx::cluster_ctarank();
   constexpr int SLICE = K / kColmaxCluster;
   for (int c = (int)rank * SLICE + threadIdx.x; c < ((int)rank + 1) * SLICE; c += P::THREADS) {
@@ -109,7 +129,9 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
     for (uint32_t r = 0; r < kColmaxCluster; ++r) m = max(m, ptx::ld_dsmem_u32(cmx + c, r));
     atomicMax(chan_max_bits + c, m);  // float bits of values >= +0 order like the floats
   }
+  trace(0, 14);
   ptx::cluster_sync();  // keep this CTA's shared memory alive until every peer has read it
+  trace(0, 15);
 }
 
 // ------------------------------------------------------------------------------ a3 - a6 (and a7)
@@ -134,10 +156,14 @@ RRS_DEVICE uint32_t operand_byte(int q, bool e4m3) {
 template <int K>
 struct QuantPlan {
   static constexpr int TPR = K / 32;                                       // threads per row, 32 codes each
-  static constexpr int R = TPR >= 64 ? 1 : 64 / TPR;                       // rows per CTA tile
+  static constexpr int R = TPR >= 256 ? 1 : 256 / TPR;                     // rows per CTA tile (8 warps)
   static constexpr int THREADS = R * TPR;
   static constexpr int TILE = R * K;                                       // f32 elements per tile
-  static constexpr int BYTES = 2 * TILE * 4 + K * 4 + 64 * 4 + 64;         // 2 stages + chan_max + red + bars
+  // TMA-bulk ring deep enough to cover the load latency (2 CTAs/SM up to K = 8192, 1 CTA/SM beyond);
+  // chan_max is staged in the first ring slot before any row load is issued
+  static constexpr int BUDGET = K <= 8192 ? 96 * 1024 : 160 * 1024;
+  static constexpr int STAGES = min_c(8, max_c(2, BUDGET / (TILE * 4)));
+  static constexpr int BYTES = STAGES * TILE * 4 + K * 4 + 64 * 4 + 8 * 8 + 64;  // ring + chan_max + red + bars
   static_assert(THREADS <= 1024 && THREADS % 32 == 0, "quant layout");
 };
 
@@ -149,8 +175,9 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
   using Q = QuantPlan<K>;
   constexpr int TPR = Q::TPR;
   extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int STAGES = Q::STAGES;
   float* stage = reinterpret_cast<float*>(smem);
-  float* cms = reinterpret_cast<float*>(smem + 2 * Q::TILE * 4);       // chan_max [K]
+  float* cms = reinterpret_cast<float*>(smem + STAGES * Q::TILE * 4);   // chan_max [K]
   float* red = cms + K;
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 64);
   const int tid = threadIdx.x;
@@ -165,11 +192,12 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
     ptx::mbar_arrive_expect_tx(&bar[buf], bytes);
     ptx::bulk_load(stage + buf * Q::TILE, Xr + tile * Q::R * K, bytes, &bar[buf]);
   };
+  trace(1, 2);
   if (tid == 0) {
-    ptx::mbar_init(&bar[0], 1);
-    ptx::mbar_init(&bar[1], 1);
+    for (int b = 0; b < STAGES; ++b) ptx::mbar_init(&bar[b], 1);
     ptx::fence_barrier_init();
   }
+  trace(1, 0);
   int pj[32];  // perm is an offline input: read it before waiting for the FWHT pass
   {
     const int4* pp = reinterpret_cast<const int4*>(perm + j0);
@@ -181,9 +209,10 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
   }
   ptx::pdl_wait();  // X~ and chan_max come from fwht_colmax_kernel
   __syncthreads();
-  if (tid == 0) {
-    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
-    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  trace(1, 1);
+  if (tid == 0) {  // start the row loads first; the s_g setup below overlaps them
+    for (int b = 0; b < STAGES; ++b)
+      if (blockIdx.x + (int64_t)b * gridDim.x < ntiles) issue(blockIdx.x + (int64_t)b * gridDim.x, b);
   }
   float inv_s = 1.0f;
   if (smooth) {
@@ -200,11 +229,13 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
     inv_s = __frcp_rn(m);     // R9: fl(1/s_g)
     if (blockIdx.x == 0 && rr == 0 && (j0 & 127) == 0 && s_group_out) s_group_out[j0 >> 7] = m;
   }
+  trace(1, 2);
 
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
-    ptx::mbar_wait(&bar[buf], (it >> 1) & 1);
+    const int buf = it % STAGES;
+    ptx::mbar_wait(&bar[buf], (it / STAGES) & 1);
+    trace(1, 3 + (it < 10 ? it : 10));
     const float* xs = stage + buf * Q::TILE + rr * K;
     float z[32];
     float m = 0.0f;
@@ -228,7 +259,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
       m = mm;
     }
     __syncthreads();  // every thread has read stage[buf] (and red): both may be reused
-    if (tid == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
+    if (tid == 0 && tile + STAGES * (int64_t)gridDim.x < ntiles) issue(tile + STAGES * (int64_t)gridDim.x, buf);
     const int64_t trow = tile * Q::R + rr;
     if (trow < T) {
       float alpha = 1.0f, r = 0.0f;
@@ -236,26 +267,50 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
         alpha = __fdiv_rn(m, 7.0f);  // stored scale alpha_t = fl(m/7)
         r = __fdiv_rn(7.0f, m);      // R9: codes use fl(7/m)
       }
-      uint32_t packed[4] = {0u, 0u, 0u, 0u};
-      uint32_t wide[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+      if (Xq == nullptr && e4m3) {
+        // hot path (rrs_linear): only the E4M3 operand.  rint (RNE) then clamp in f32 -- the same integer
+        // as __float2int_rn + clamp -- and one cvt per pair (integers of magnitude <= 8 are exact in E4M3).
+        uint32_t w[8];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        int q = __float2int_rn(__fmul_rn(z[k], r));  // R10: round half to even
-        q = max(-8, min(7, q));                      // R11
-        packed[k >> 3] |= (uint32_t)(q & 0xF) << ((k & 7) * 4);
-        wide[k >> 2] |= operand_byte(q, e4m3 != 0) << ((k & 3) * 8);
-      }
-      if (Xq) {
-        *reinterpret_cast<uint4*>(Xq + trow * (K / 2) + j0 / 2) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-      }
-      if (Xq8) {
+        for (int k = 0; k < 32; k += 4) {
+          float q[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h)  // R10, R11; "+ 0" turns rint's -0 into the canonical +0 (code byte 0x00)
+            q[h] = __fadd_rn(fminf(fmaxf(rintf(__fmul_rn(z[k + h], r)), -8.0f), 7.0f), 0.0f);
+          uint32_t lo, hi;
+          asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
+              : "=r"(lo) : "f"(q[1]), "f"(q[0]));
+          asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
+              : "=r"(hi) : "f"(q[3]), "f"(q[2]));
+          w[k >> 2] = lo | (hi << 16);
+        }
         uint4* dst = reinterpret_cast<uint4*>(Xq8 + trow * K + j0);
-        dst[0] = make_uint4(wide[0], wide[1], wide[2], wide[3]);
-        dst[1] = make_uint4(wide[4], wide[5], wide[6], wide[7]);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      } else {
+        uint32_t packed[4] = {0u, 0u, 0u, 0u};
+        uint32_t wide[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          int q = __float2int_rn(__fmul_rn(z[k], r));  // R10: round half to even
+          q = max(-8, min(7, q));                      // R11
+          packed[k >> 3] |= (uint32_t)(q & 0xF) << ((k & 7) * 4);
+          wide[k >> 2] |= operand_byte(q, e4m3 != 0) << ((k & 3) * 8);
+        }
+        if (Xq) {
+          *reinterpret_cast<uint4*>(Xq + trow * (K / 2) + j0 / 2) =
+              make_uint4(packed[0], packed[1], packed[2], packed[3]);
+        }
+        if (Xq8) {
+          uint4* dst = reinterpret_cast<uint4*>(Xq8 + trow * K + j0);
+          dst[0] = make_uint4(wide[0], wide[1], wide[2], wide[3]);
+          dst[1] = make_uint4(wide[4], wide[5], wide[6], wide[7]);
+        }
       }
       if (j0 == 0) scale_out[trow] = alpha;
     }
   }
+  trace(1, 15);
   ptx::pdl_launch_dependents();
 }
 
@@ -293,9 +348,22 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
   const int smem = ColmaxSmem<K>::BYTES;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  int grid = grid_for(kern, P::THREADS, smem, (T + P::R - 1) / P::R, nsm);
-  if (grid == 0) return cudaSuccess;
-  grid = (grid + kColmaxCluster - 1) / kColmaxCluster * kColmaxCluster;  // whole clusters (idle CTAs are fine)
+  // persistent: only as many clusters as can be co-resident (a cluster of 8 must fit in one GPC, so this is
+  // below SMs x CTAs-per-SM / 8); late clusters would otherwise run as a second wave
+  static int max_clusters[2] = {0, 0};  // per K instantiation, cached
+  if (max_clusters[0] == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kColmaxCluster * 1024);
+    cfg.blockDim = dim3(P::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = nsm / kColmaxCluster;
+    max_clusters[0] = n;
+  }
+  const int64_t tiles = (T + P::R - 1) / P::R;
+  if (tiles == 0) return cudaSuccess;
+  const int64_t clusters = std::min<int64_t>(max_clusters[0], (tiles + kColmaxCluster - 1) / kColmaxCluster);
+  const int grid = (int)clusters * kColmaxCluster;  // whole clusters (CTAs without a tile are fine)
   kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr);
   return cudaGetLastError();
 }

@@ -135,6 +135,12 @@ RRS_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
   return r;
 }
+// arrive on an mbarrier given by its shared::cluster address (may be a peer CTA's); release at CTA scope
+// (no cluster-wide memory fence: enough when the arrive only has to order tcgen05.ld completions)
+RRS_DEV void mbar_arrive_remote(uint32_t bar_cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
+}
+// same with release at cluster scope (orders this thread's prior tcgen05.st for a peer CTA's MMA)
 RRS_DEV void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }

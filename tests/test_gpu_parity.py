@@ -45,7 +45,12 @@ def _run_prologue(X_bits, perm, i8=False):
     sg = torch.empty(K // 128, dtype=torch.float32, device=DEV)
     cm = torch.empty(K, dtype=torch.float32, device=DEV)
     rrs.rrs_rotate_smooth_quant(X, p, Xq, Xop, xs, sg, chan_max=cm, i8=i8)
+    # the operand-only call (Xq = NULL) is the rrs_linear hot path, which takes a separate code path in the
+    # quantisation kernel: its bytes must be identical
+    Xop2 = torch.empty_like(Xop)
+    rrs.rrs_rotate_smooth_quant(X, p, None, Xop2, torch.empty_like(xs), torch.empty_like(sg), i8=i8)
     torch.cuda.synchronize()
+    assert torch.equal(Xop, Xop2)
     return dict(Xq=Xq.cpu().numpy(), Xop=Xop.cpu().numpy(), Xq8=decode_operand(Xop.cpu().numpy(), i8),
                 alpha=xs.cpu().numpy(), s_group=sg.cpu().numpy(), chan_max=cm.cpu().numpy())
 
@@ -181,7 +186,9 @@ def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile, i8):
     Yf_np = Yf.cpu().numpy()
     assert np.isnan(Yf_np[:, N:]).all()  # nothing written past N
     assert y_normalised_error(Yf_np[:, :N], ref) <= 1e-5
-    assert bf16_ulp_error(Yb[:, :N].float().cpu().numpy(), ref["Y"]) <= 1.0
+    assert bf16_ulp_error(Yb[:, :N].float().cpu().numpy(), ref["Y"], ref) <= 1.0
+    # bf16 output is the round-to-nearest-even of the very same f32 accumulation
+    assert torch.equal(Yb[:, :N], Yf[:, :N].to(torch.bfloat16))
 
 
 @pytest.mark.parametrize("T", [130, 100])
@@ -219,7 +226,8 @@ def test_rrs_linear_end_to_end(wl, T, N, i8):
     assert np.array_equal(layer.Wq.cpu().numpy(), ref["Wq"])
     assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
     Yb = layer(dev_bf16(X_bits), out_dtype=torch.bfloat16)
-    assert bf16_ulp_error(Yb.float().cpu().numpy(), ref["Y"]) <= 1.0
+    assert bf16_ulp_error(Yb.float().cpu().numpy(), ref["Y"], ref) <= 1.0
+    assert torch.equal(Yb, Y.to(torch.bfloat16))  # RNE of the same f32 accumulation
 
 
 def test_rrs_linear_equals_prologue_plus_gemm_bitwise():
