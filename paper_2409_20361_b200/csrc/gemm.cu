@@ -260,35 +260,62 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         const float s = kPlain ? 1.0f : s_sm[g];
         const float2 s2 = make_float2(s, s);
         const uint32_t tbase = tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS;
+        if constexpr (kFp8 && !kDebug) {
+          // software-pipelined: chunk c+1 is in flight while chunk c is accumulated; the buffer is released
+          // as soon as the last chunk has landed in registers
+          constexpr int NCH = EPI_COLS / 16;
+          uint32_t ra[16], rb[16];
+          RRS_TMEM_LD16(tbase, ra);
+          RRS_TMEM_WAIT_LD16(ra);
 #pragma unroll
-        for (int cc = 0; cc < EPI_COLS / 16; ++cc) {
-          uint32_t r[16];
-          RRS_TMEM_LD16(tbase + cc * 16, r);
-          ptx::tmem_ld_wait();
-          if constexpr (kFp8) {
-            if (cc == EPI_COLS / 16 - 1) {
-              // every column of this buffer is in registers: release it before the last chunk's math
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+          for (int cc = 0; cc < NCH; ++cc) {
+            uint32_t(&cur)[16] = (cc & 1) ? rb : ra;
+            uint32_t(&nxt)[16] = (cc & 1) ? ra : rb;
+            if (cc + 1 < NCH) RRS_TMEM_LD16(tbase + (cc + 1) * 16, nxt);
+#pragma unroll
+            for (int j = 0; j < 8; ++j)  // acc += s_g * P_g (R14); the FP8 carrier's P_g is an exact float
+              acc2[cc * 8 + j] = __ffma2_rn(s2, make_float2(__uint_as_float(cur[2 * j]), __uint_as_float(cur[2 * j + 1])),
+                                            acc2[cc * 8 + j]);
+            if (cc + 1 < NCH) {
+              RRS_TMEM_WAIT_LD16(nxt);
+              if (cc + 2 == NCH) {  // all chunks of this buffer are in registers: release it
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+              }
             }
           }
-          if (kDebug && row < p.T) {
-            const int gg = kPlain ? 0 : g;
+        } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int n = col0 + cc * 16 + j;
-              const int32_t P = kFp8 ? __float2int_rn(__uint_as_float(r[j])) : (int32_t)(r[j] - kBias);
-              if (n < p.N) p.P_debug[((int64_t)gg * p.T + row) * p.N + n] = P;
+          for (int cc = 0; cc < EPI_COLS / 16; ++cc) {
+            uint32_t r[16];
+            RRS_TMEM_LD16(tbase + cc * 16, r);
+            RRS_TMEM_WAIT_LD16(r);
+            if constexpr (kFp8) {
+              if (cc == EPI_COLS / 16 - 1) {
+                // every column of this buffer is in registers: release it before the last chunk's math
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+              }
             }
-          }
+            if (kDebug && row < p.T) {
+              const int gg = kPlain ? 0 : g;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float2 f = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-            // int8 carrier: (1.5*2^23 + P) - 1.5*2^23 = P exactly for |P| < 2^22; FP8 carrier: P is already
-            // an exact float.  Then acc += s_g * P (R14).
-            if constexpr (!kFp8) f = __fadd2_rn(f, neg_bias2);
-            acc2[cc * 8 + j] = __ffma2_rn(s2, f, acc2[cc * 8 + j]);
+              for (int j = 0; j < 16; ++j) {
+                const int n = col0 + cc * 16 + j;
+                const int32_t P = kFp8 ? __float2int_rn(__uint_as_float(r[j])) : (int32_t)(r[j] - kBias);
+                if (n < p.N) p.P_debug[((int64_t)gg * p.T + row) * p.N + n] = P;
+              }
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float2 f = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+              // int8 carrier: (1.5*2^23 + P) - 1.5*2^23 = P exactly for |P| < 2^22; FP8 carrier: P is already
+              // an exact float.  Then acc += s_g * P (R14).
+              if constexpr (!kFp8) f = __fadd2_rn(f, neg_bias2);
+              acc2[cc * 8 + j] = __ffma2_rn(s2, f, acc2[cc * 8 + j]);
+            }
           }
         }
         if constexpr (!kFp8) {

@@ -223,6 +223,16 @@ RRS_DEV void mma_commit(uint64_t* bar) {
         "=r"(r[15])                                                                                     \
       : "r"(taddr))
 
+// tcgen05.wait::ld that also "redefines" the 16 destination registers of the preceding RRS_TMEM_LD16, so
+// the compiler cannot schedule their uses above the wait
+#define RRS_TMEM_WAIT_LD16(r)                                                                            \
+  asm volatile("tcgen05.wait::ld.sync.aligned;"                                                          \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),     \
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), \
+                 "+r"(r[14]), "+r"(r[15])                                                                \
+               :                                                                                         \
+               : "memory")
+
 #define RRS_TMEM_ST32_SPLAT(taddr, v)                                                                    \
   asm volatile(                                                                                         \
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"   \
