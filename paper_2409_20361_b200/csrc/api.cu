@@ -134,6 +134,32 @@ static rrs_status gather_columns(const void* shard, int64_t T, int64_t N_total, 
 }
 
 
+namespace rrs {
+cudaError_t prepare_kernel_impl(const void* fn, int smem, int threads, int* blocks_per_sm) {
+  static std::mutex mu;
+  static KernelPrep cache[256];
+  static int n = 0;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < n; ++i) {
+    if (cache[i].fn == fn && cache[i].dev == dev) {
+      if (blocks_per_sm) *blocks_per_sm = cache[i].per_sm;
+      return cudaSuccess;
+    }
+  }
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  if (n < 256) cache[n++] = KernelPrep{fn, dev, per_sm};
+  if (blocks_per_sm) *blocks_per_sm = per_sm;
+  return cudaSuccess;
+}
+}  // namespace rrs
+
 extern "C" {
 
 const char* rrs_status_str(int s) {

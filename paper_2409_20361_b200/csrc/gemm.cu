@@ -37,6 +37,22 @@
 
 namespace rrs {
 
+// Optional timeline (bench/micro/gemm_trace.cu builds this file with -DRRS_TRACE): %globaltimer at fixed
+// points of the first tile's first 16 groups, per CTA: [0] MMA after tempty wait, [1] after full wait,
+// [2] after issue; [3]/[4] first promotion warp after tfull wait / after release; [5]/[6] last warp.
+#ifdef RRS_TRACE
+__device__ unsigned long long g_gtrace[160][16][8];
+__device__ __forceinline__ void gtrace(int g, int slot) {
+  if (blockIdx.x < 160 && g < 16) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_gtrace[blockIdx.x][g][slot] = t;
+  }
+}
+#else
+__device__ __forceinline__ void gtrace(int, int) {}
+#endif
+
 namespace gemm {
 constexpr int BM = 128;        // tokens per CTA    (TMEM lanes)
 constexpr int BN = 240;        // outputs per tile  (TMEM columns per accumulator; 256-column slots)
@@ -81,7 +97,9 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   using C = Cfg<kCta>;
   constexpr int STAGES = C::STAGES, A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-byte alignment (SWIZZLE_128B atoms) by offsetting the shared array itself, so the compiler keeps
+  // the shared address space for every pointer derived from it (LDS/STS, not generic loads)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
@@ -153,51 +171,55 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (pair leader)
+    // one thread runs the whole loop: no warp-synchronous step between the barrier waits and the issue
     constexpr uint32_t idesc = kFp8 ? ptx::idesc_e4m3(BM * kCta, BN) : ptx::idesc_i8(BM * kCta, BN);
     int stage = 0;
     uint32_t phase = 0;
     uint32_t acc_iter = 0;  // number of accumulator buffers filled so far
-    for (int tile = blockIdx.x / kCta; leader && tile < p.num_tiles; tile += gridDim.x / kCta) {
+    const uint64_t a_desc0 = ptx::smem_desc_sw128(sA), b_desc0 = ptx::smem_desc_sw128(sB);
+    for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
       for (int kb = 0; kb < p.G; ++kb) {
         const uint32_t b = acc_iter & 1;
         if (kPlain ? kb == 0 : true) {
           // use u = acc_iter >> 1 of buffer b needs the (u)-th release (completion #u of tempty[b]); the
           // releases come from both CTAs of a pair (cluster-scope acquire)
           if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
-          else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
+          else ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
         }
-        ptx::mbar_wait(&full[stage], phase);
+        if (tile == (int)blockIdx.x / kCta) gtrace(kb, 0);
+        ptx::mbar_wait_spin(&full[stage], phase);
+        if (tile == (int)blockIdx.x / kCta) gtrace(kb, 1);
         ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          const uint64_t a_desc = ptx::smem_desc_sw128(sA + stage * A_BYTES);
-          const uint64_t b_desc = ptx::smem_desc_sw128(sB + stage * B_BYTES);
-          const uint32_t d = tmem_base + b * ACC_STRIDE;
+        // descriptor start addresses advance in 16-byte units: stage offsets, then 32 bytes per K step
+        const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
+        const uint64_t b_desc = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
+        const uint32_t d = tmem_base + b * ACC_STRIDE;
 #pragma unroll
-          for (int k = 0; k < BK / 32; ++k) {
-            // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier:
-            // always accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
-            if constexpr (kFp8) {
-              const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (k > 0);
-              if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
-              else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
-            } else {
-              if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
-              else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
-            }
-          }
-          if constexpr (kCta == 1) {
-            ptx::mma_commit(&empty[stage]);
-            if (!kPlain || kb == p.G - 1) ptx::mma_commit(&tfull[b]);
+        for (int k = 0; k < BK / 32; ++k) {
+          // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier:
+          // always accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
+          if constexpr (kFp8) {
+            const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (k > 0);
+            if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
+            else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
           } else {
-            ptx::mma_commit_pair(&empty[stage], 0x3);
-            if (!kPlain || kb == p.G - 1) ptx::mma_commit_pair(&tfull[b], 0x3);
+            if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
+            else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
           }
         }
-        __syncwarp();
+        if constexpr (kCta == 1) {
+          ptx::mma_commit(&empty[stage]);
+          if (!kPlain || kb == p.G - 1) ptx::mma_commit(&tfull[b]);
+        } else {
+          ptx::mma_commit_pair(&empty[stage], 0x3);
+          if (!kPlain || kb == p.G - 1) ptx::mma_commit_pair(&tfull[b], 0x3);
+        }
+        if (tile == (int)blockIdx.x / kCta) gtrace(kb, 2);
         if (!kPlain || kb == p.G - 1) ++acc_iter;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
+    __syncwarp();
   } else {
     // ------------------------------------------------------------------ promotion + epilogue
     constexpr uint32_t kBias = 0x4B400000u;  // bits of 1.5 * 2^23
@@ -255,8 +277,12 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       const int ngroups = kPlain ? 1 : p.G;
       for (int g = 0; g < ngroups; ++g) {
         const uint32_t b = acc_iter & 1;
-        ptx::mbar_wait(&tfull[b], (acc_iter >> 1) & 1);
+        // RRS: a buffer lands every group, spin for the lowest wake-up latency; plain: once per tile, sleep
+        if constexpr (kPlain) ptx::mbar_wait(&tfull[b], (acc_iter >> 1) & 1);
+        else ptx::mbar_wait_spin(&tfull[b], (acc_iter >> 1) & 1);
         ptx::tc_fence_after();
+        const bool trace_me = tile == (int)blockIdx.x / kCta && lane == 0 && (ew == 0 || ew == NUM_EPI_WARPS - 1);
+        if (trace_me) gtrace(g, ew == 0 ? 3 : 5);
         const float s = kPlain ? 1.0f : s_sm[g];
         const float2 s2 = make_float2(s, s);
         const uint32_t tbase = tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS;
@@ -282,6 +308,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+                if (trace_me) gtrace(g, ew == 0 ? 4 : 6);
               }
             }
           }
@@ -422,7 +449,7 @@ static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, 
                                   cudaStream_t st) {
   auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug, kCta, kFp8>;
   constexpr int smem = gemm::Cfg<kCta>::SMEM_BYTES;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = prepare_kernel(kern, smem, gemm::THREADS);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);

@@ -5,8 +5,18 @@
 
 namespace rrs {
 
-// launch with programmatic dependent launch enabled: the kernel may start while the previous kernel in
-// the stream drains; it calls griddepcontrol.wait before touching that kernel's outputs.
+// Per-(kernel, device) one-time setup: the dynamic shared-memory opt-in and the occupancy query are host
+// calls that cost microseconds; do them once per kernel function and device, not on every launch.
+struct KernelPrep {
+  const void* fn;
+  int dev, per_sm;
+};
+cudaError_t prepare_kernel_impl(const void* fn, int smem, int threads, int* blocks_per_sm);
+template <class F>
+cudaError_t prepare_kernel(F kern, int smem, int threads, int* blocks_per_sm = nullptr) {
+  return prepare_kernel_impl(reinterpret_cast<const void*>(kern), smem, threads, blocks_per_sm);
+}
+
 template <class... KArgs, class... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int threads, int smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};

@@ -335,8 +335,7 @@ __global__ void perm_rank_kernel(const float* __restrict__ c, int K, int32_t* __
 template <class F>
 static int grid_for(F kern, int threads, int smem, int64_t tiles, int nsm) {
   int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-  if (per_sm < 1) per_sm = 1;
+  prepare_kernel(kern, smem, threads, &per_sm);
   return (int)std::min<int64_t>(tiles, (int64_t)nsm * per_sm);
 }
 
@@ -346,7 +345,7 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
   using P = FwhtPlan<K>;
   auto kern = fwht_colmax_kernel<K>;
   const int smem = ColmaxSmem<K>::BYTES;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = prepare_kernel(kern, smem, P::THREADS);
   if (e != cudaSuccess) return e;
   // persistent: only as many clusters as can be co-resident (a cluster of 8 must fit in one GPC, so this is
   // below SMs x CTAs-per-SM / 8); late clusters would otherwise run as a second wave
@@ -374,7 +373,7 @@ static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* per
                                   cudaStream_t st) {
   using Q = QuantPlan<K>;
   auto kern = smooth_quant_kernel<K>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Q::BYTES);
+  cudaError_t e = prepare_kernel(kern, Q::BYTES, Q::THREADS);
   if (e != cudaSuccess) return e;
   // persistent: at most 2 CTAs per SM, so the per-CTA setup (chan_max load, s_g) is amortised over many rows
   int grid = (int)std::min<int64_t>(grid_for(kern, Q::THREADS, Q::BYTES, (T + Q::R - 1) / Q::R, nsm), 2 * nsm);

@@ -68,6 +68,18 @@ RRS_DEV uint32_t ld_dsmem_u32(const void* p, uint32_t rank) {
 RRS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 RRS_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// latency-critical wait: spin on try_wait without a suspend-time hint (the waiting warp has nothing else to
+// do, and a suspended warp wakes up later than a spinning one)
+RRS_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 // wait with cluster-scope acquire: pairs with mbarrier.arrive.release.cluster from a peer CTA
 RRS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
   asm volatile(
