@@ -41,6 +41,8 @@ int main(int argc, char** argv) {
       auto f = [&](int s) { return h[c][g][s] ? (long long)(h[c][g][s] - t0) : -1LL; };
       printf("  %2d: %6lld %6lld %6lld | %6lld %6lld | %6lld %6lld\n", g, f(0), f(1), f(2), f(3), f(4), f(5), f(6));
     }
+    if (h[c][14][7]) printf("  first tile epilogue: %lld -> %lld ns (%lld ns)\n", (long long)(h[c][14][7] - t0),
+                            (long long)(h[c][15][7] - t0), (long long)(h[c][15][7] - h[c][14][7]));
   }
   return 0;
 }

@@ -24,7 +24,23 @@ int main(int argc, char** argv) {
   cudaMalloc(&q, T * K); cudaMalloc(&sc, T * 4); cudaMalloc(&perm, K * 4);
   cudaMemcpy(X, hx.data(), T * K * 2, cudaMemcpyHostToDevice);
   cudaMemcpy(perm, hp.data(), K * 4, cudaMemcpyHostToDevice);
-  for (int rep = 0; rep < 3; ++rep) {
+  unsigned* counter;
+  cudaMalloc(&counter, 256);
+  const bool fused = argc > 3 && atoi(argv[3]) != 0;
+  for (int rep = 0; rep < 3 && fused; ++rep) {
+    cudaMemset(cm, 0, K * 4);
+    cudaMemset(counter, 0, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    rrs::launch_prologue_fused(X, T, K, cm, Xr, counter, perm, sg, nullptr, q, sc, true, nsm, 0);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaDeviceSynchronize();
+    float a;
+    cudaEventElapsedTime(&a, e0, e1);
+    printf("rep %d: %s fused prologue %.1f us\n", rep, cudaGetErrorString(e), a * 1e3);
+  }
+  for (int rep = 0; rep < 3 && !fused; ++rep) {
     cudaMemset(cm, 0, K * 4);
     cudaEvent_t e0, e1, e2;
     cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);

@@ -100,7 +100,7 @@ size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t
   Workspace tmp;
   Workspace& ws = w ? *w : tmp;
   ws.Xr = static_cast<float*>(take(sizeof(float) * (size_t)T * K));
-  ws.chan_max = static_cast<float*>(take(sizeof(float) * K));
+  ws.chan_max = static_cast<float*>(take(sizeof(float) * (K + 64)));  // [K] + the fused prologue's CTA counter
   ws.s_group = static_cast<float*>(take(sizeof(float) * (K / group)));
   ws.x_scale = static_cast<float*>(take(sizeof(float) * (T > 0 ? T : 1)));
   ws.Xq8 = static_cast<int8_t*>(take((size_t)T * K));
@@ -229,10 +229,18 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
 }
 
 static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* perm, uint8_t* Xq, int8_t* Xq8,
-                           float* x_scale, float* s_group, float* chan_max, float* Xr, bool e4m3, int nsm,
-                           cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * K, st);
+                           float* x_scale, float* s_group, float* chan_max, unsigned* counter, float* Xr, bool e4m3,
+                           int nsm, cudaStream_t st) {
+  // chan_max (and the fused kernel's CTA counter) start at zero; one memset when they are contiguous
+  const bool contiguous = reinterpret_cast<unsigned*>(chan_max) + K == counter;
+  cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * (contiguous ? K + 1 : K), st);
+  if (e == cudaSuccess && !contiguous) e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
+  if (T > 0 && rrs::prologue_fused_supports_k(K)) {
+    e = rrs::launch_prologue_fused(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
+                                   counter, perm, s_group, Xq, Xq8, x_scale, e4m3, nsm, st);
+    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_fused_kernel");
+  }
   e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
                               nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "fwht_colmax_kernel");
@@ -260,8 +268,8 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   if (!chan_max) chan_max = w.chan_max;
-  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, w.Xr, (flags & RRS_OPERAND_I8) == 0, nsm,
-                  static_cast<cudaStream_t>(stream));
+  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, reinterpret_cast<unsigned*>(w.chan_max) + K,
+                  w.Xr, (flags & RRS_OPERAND_I8) == 0, nsm, static_cast<cudaStream_t>(stream));
 }
 
 static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int8_t* Wq8, const float* w_scale,
@@ -317,7 +325,8 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, w.Xr, e4m3, nsm, st))
+  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max,
+                              reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, e4m3, nsm, st))
     return s;
   if (T == 0) return RRS_OK;
   const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m

@@ -262,14 +262,15 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
       const int row = m_blk * BM * kCta + (int)rank * BM + row_in_tile;
       const int col0 = n_blk * BN + half * EPI_COLS;
-      // stage beta for this tile (named barrier among the 256 epilogue threads)
-      asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
-      if (p.w_scale) {
+      // the epilogue's scales are loaded now and only consumed after the last group, so their global-memory
+      // latency is hidden behind the whole K loop
+      float beta_pref = 0.0f, xs_pref = 0.0f;
+      {
         const int c = threadIdx.x - 64;
         const int n = n_blk * BN + c;
-        if (c < BN) beta_sm[c] = (n < p.N) ? p.w_scale[n] : 0.0f;
+        if (p.w_scale && c < BN && n < p.N) beta_pref = __ldg(p.w_scale + n);
+        if (p.x_scale && row < p.T) xs_pref = __ldg(p.x_scale + row);
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
 
       float2 acc2[EPI_COLS / 2];  // acc pairs (columns 2i, 2i+1 of this thread's EPI_COLS)
 #pragma unroll
@@ -362,8 +363,14 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         acc[2 * c + 1] = acc2[c].y;
       }
       // ---- epilogue: Y = acc * (alpha_t * out_scale) * beta_n
+      const bool trace_epi = tile == (int)blockIdx.x / kCta && lane == 0 && ew == 0;
+      if (trace_epi) gtrace(14, 7);
+      // stage this tile's beta (named barrier among the epilogue threads: the previous tile's readers are done)
+      asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
+      if (threadIdx.x - 64 < BN) beta_sm[threadIdx.x - 64] = beta_pref;
+      asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
       if (p.Y != nullptr && row < p.T) {
-        const float rs = p.x_scale[row] * p.out_scale;
+        const float rs = xs_pref * p.out_scale;
         if constexpr (kF32Out) {
           float* yrow = reinterpret_cast<float*>(p.Y) + (int64_t)row * p.ldy;
 #pragma unroll
@@ -405,6 +412,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           }
         }
       }
+      if (trace_epi) gtrace(15, 7);
     }
   }
   ptx::tc_fence_before();

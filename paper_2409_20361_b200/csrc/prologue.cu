@@ -40,18 +40,20 @@ struct ColmaxSmem {
   using P = FwhtPlan<K>;
   static constexpr int TILE_D = ((P::TILE_PAD * 8 + 127) / 128) * 128;  // padded fp64 transpose tile
   static constexpr int STAGE = P::TILE * 2;     // one bf16 tile
-  static constexpr int BYTES = TILE_D + 2 * STAGE + 64;
+  static constexpr int BYTES = TILE_D + 2 * STAGE + 64 + 64 * 4;  // + 5 barriers (40 B), reduction scratch
+  static_assert(2 * P::TILE * 4 <= TILE_D && K * 4 <= 2 * STAGE, "fused quantisation staging");
 };
 
 constexpr int kColmaxCluster = 8;  // CTAs that combine their column maxima through DSMEM before the atomics
 
-template <int K>
-__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
-fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
-                   float* __restrict__ Xr) {
+// The FWHT pass (rows a1-a2): every CTA of the (persistent, clustered) grid transforms its rows, writes X~
+// f32 and, unless chan_max_bits is null, folds its column maxima into chan_max (DSMEM cluster reduction +
+// one atomicMax per column per cluster).  Ends with a cluster barrier.  Every thread must call it.
+template <int K, bool kFinalClusterSync = true>
+RRS_DEVICE void fwht_phase(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
+                           float* __restrict__ Xr, uint8_t* smem) {
   using P = FwhtPlan<K>;
   using S = ColmaxSmem<K>;
-  extern __shared__ __align__(128) uint8_t smem[];
   double* sm = reinterpret_cast<double*>(smem);
   uint16_t* stage = reinterpret_cast<uint16_t*>(smem + S::TILE_D);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::TILE_D + 2 * S::STAGE);
@@ -65,8 +67,7 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
     ptx::bulk_load(stage + buf * P::TILE, X + tile * P::R * K, bytes, &bar[buf]);
   };
   if (threadIdx.x == 0) {
-    ptx::mbar_init(&bar[0], 1);
-    ptx::mbar_init(&bar[1], 1);
+    for (int b = 0; b < 5; ++b) ptx::mbar_init(&bar[b], 1);  // [0,1] this pass; [2..4] the fused quant pass
     ptx::fence_barrier_init();
   }
   __syncthreads();
@@ -123,15 +124,36 @@ fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restri
   trace(0, 13);
   const uint32_t rank = ptx::cluster_ctarank();
   constexpr int SLICE = K / kColmaxCluster;
-  for (int c = (int)rank * SLICE + threadIdx.x; c < ((int)rank + 1) * SLICE; c += P::THREADS) {
-    uint32_t m = 0u;
+  constexpr int PER_THREAD = (SLICE + P::THREADS - 1) / P::THREADS;
+  uint32_t mx[PER_THREAD];
 #pragma unroll
-    for (uint32_t r = 0; r < kColmaxCluster; ++r) m = max(m, ptx::ld_dsmem_u32(cmx + c, r));
-    atomicMax(chan_max_bits + c, m);  // float bits of values >= +0 order like the floats
+  for (int i = 0; i < PER_THREAD; ++i) {  // all 8 x PER_THREAD remote loads in flight at once
+    const int c = (int)rank * SLICE + threadIdx.x + i * P::THREADS;
+    uint32_t m = 0u;
+    if (threadIdx.x + i * P::THREADS < SLICE) {
+#pragma unroll
+      for (uint32_t r = 0; r < kColmaxCluster; ++r) m = max(m, ptx::ld_dsmem_u32(cmx + c, r));
+    }
+    mx[i] = m;
+  }
+#pragma unroll
+  for (int i = 0; i < PER_THREAD; ++i) {
+    const int c = (int)rank * SLICE + threadIdx.x + i * P::THREADS;
+    if (threadIdx.x + i * P::THREADS < SLICE) atomicMax(chan_max_bits + c, mx[i]);  // float bits of values >= +0
   }
   trace(0, 14);
-  ptx::cluster_sync();  // keep this CTA's shared memory alive until every peer has read it
+  // keep this CTA's shared memory alive until every peer has read it (the fused kernel's grid barrier,
+  // which starts with a cluster barrier, provides the same guarantee)
+  if constexpr (kFinalClusterSync) ptx::cluster_sync();
   trace(0, 15);
+}
+
+template <int K>
+__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
+fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
+                   float* __restrict__ Xr) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  fwht_phase<K>(X, T, chan_max_bits, Xr, smem);
 }
 
 // ------------------------------------------------------------------------------ a3 - a6 (and a7)
@@ -151,6 +173,191 @@ RRS_DEVICE uint32_t operand_byte(int q, bool e4m3) {
   const uint32_t m = ((a << 3) >> e) & 7u;           // 3 fraction bits
   const uint32_t mag = a ? (((e + 7u) << 3) | m) : 0u;  // exponent bias 7
   return mag | (q < 0 ? 0x80u : 0u);
+}
+
+
+// ------------------------------------------------------------------------------ a3 - a6 building blocks
+
+// This thread's 32 reordered positions j0..j0+31 -> perm entries (an offline input).
+RRS_DEVICE void load_perm32(const int32_t* __restrict__ perm, int j0, int (&pj)[32]) {
+  const int4* pp = reinterpret_cast<const int4*>(perm + j0);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int4 w = __ldg(pp + q);
+    pj[4 * q] = w.x; pj[4 * q + 1] = w.y; pj[4 * q + 2] = w.z; pj[4 * q + 3] = w.w;
+  }
+}
+
+// s_g = max_{j' in g} c[perm[j']] (the 4 consecutive threads of a 128-wide group) from chan_max staged
+// in shared memory; 0 -> 1 (R8); returns fl(1/s_g) (R9).  CTA 0's first tile row publishes s_group.
+RRS_DEVICE float group_inv_scale(const float* cms, const int (&pj)[32], int j0, bool publish, float* s_group_out) {
+  float m = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) m = fmaxf(m, cms[pj[k]]);
+  m = seg_max(m, 4);
+  if (m == 0.0f) m = 1.0f;
+  if (publish && (j0 & 127) == 0 && s_group_out) s_group_out[j0 >> 7] = m;
+  return __frcp_rn(m);
+}
+
+// Quantise this thread's 32 positions of one row held in shared memory (xs = the row's f32 values in natural
+// column order): Z = X~[perm] * inv_s (Eq. 2, R9), per-token absmax over the TPR threads of the row,
+// alpha = fl(m/7), codes rint_even(fl(Z * fl(7/m))) clamped to [-8, 7] (R9-R11), packed nibbles and
+// operand bytes.  Contains __syncthreads() when TPR > 32 (every thread of the CTA must call it);
+// `after_reads` runs once every thread has finished reading xs (the caller recycles the buffer there).
+template <int TPR, class F>
+RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, bool smooth, float* red, int tid, int rr,
+                          int64_t trow, int64_t T, int K, int j0, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
+                          float* __restrict__ scale_out, bool e4m3, F after_reads) {
+  float z[32];
+  float m = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const float x = xs[pj[k]];
+    z[k] = smooth ? __fmul_rn(x, inv_s) : x;
+    m = fmaxf(m, fabsf(z[k]));
+  }
+  if constexpr (TPR <= 32) {
+    m = seg_max(m, TPR);
+  } else {
+    m = seg_max(m, 32);
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    const int w0 = (rr * TPR) >> 5;
+    float mm = 0.0f;
+#pragma unroll 4
+    for (int w = 0; w < TPR / 32; ++w) mm = fmaxf(mm, red[w0 + w]);
+    m = mm;
+  }
+  __syncthreads();  // every thread has read xs (and red): both may be reused
+  after_reads();
+  if (trow >= T) return;
+  float alpha = 1.0f, r = 0.0f;
+  if (m > 0.0f) {
+    alpha = __fdiv_rn(m, 7.0f);  // stored scale alpha_t = fl(m/7)
+    r = __fdiv_rn(7.0f, m);      // R9: codes use fl(7/m)
+  }
+  if (Xq == nullptr && e4m3) {
+    // hot path (rrs_linear): only the E4M3 operand.  rint (RNE) then clamp in f32 -- the same integer as
+    // __float2int_rn + clamp -- and one cvt per pair (integers of magnitude <= 8 are exact in E4M3).
+    uint32_t w[8];
+#pragma unroll
+    for (int k = 0; k < 32; k += 4) {
+      float q[4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)  // R10, R11; "+ 0" turns rint's -0 into the canonical +0 (code byte 0x00)
+        q[h] = __fadd_rn(fminf(fmaxf(rintf(__fmul_rn(z[k + h], r)), -8.0f), 7.0f), 0.0f);
+      uint32_t lo, hi;
+      asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
+          : "=r"(lo) : "f"(q[1]), "f"(q[0]));
+      asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
+          : "=r"(hi) : "f"(q[3]), "f"(q[2]));
+      w[k >> 2] = lo | (hi << 16);
+    }
+    uint4* dst = reinterpret_cast<uint4*>(Xq8 + trow * K + j0);
+    dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+  } else {
+    uint32_t packed[4] = {0u, 0u, 0u, 0u};
+    uint32_t wide[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      int q = __float2int_rn(__fmul_rn(z[k], r));  // R10: round half to even
+      q = max(-8, min(7, q));                      // R11
+      packed[k >> 3] |= (uint32_t)(q & 0xF) << ((k & 7) * 4);
+      wide[k >> 2] |= operand_byte(q, e4m3) << ((k & 3) * 8);
+    }
+    if (Xq) {
+      *reinterpret_cast<uint4*>(Xq + trow * (K / 2) + j0 / 2) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    }
+    if (Xq8) {
+      uint4* dst = reinterpret_cast<uint4*>(Xq8 + trow * K + j0);
+      dst[0] = make_uint4(wide[0], wide[1], wide[2], wide[3]);
+      dst[1] = make_uint4(wide[4], wide[5], wide[6], wide[7]);
+    }
+  }
+  if (j0 == 0) scale_out[trow] = alpha;
+}
+
+// Fused runtime prologue for K = 2^m (rows a1-a6 in one persistent launch): the FWHT pass above, a grid-wide
+// barrier (the grid is sized to be co-resident: max active clusters), then the quantisation pass on the same
+// CTAs and the same rows (their X~ is still in L2).  `counter` (next to chan_max, zeroed with it) counts CTAs.
+template <int K>
+__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
+prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
+                      float* __restrict__ Xr, unsigned* __restrict__ counter, const int32_t* __restrict__ perm,
+                      float* __restrict__ s_group_out, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
+                      float* __restrict__ scale_out, int e4m3) {
+  using P = FwhtPlan<K>;
+  using S = ColmaxSmem<K>;
+  static_assert(P::kPow2 && P::E == 32, "fused prologue: 2^m plans (32 positions per thread in both passes)");
+  constexpr int TPR = K / 32;  // quantisation threads per row == FWHT threads per row
+  extern __shared__ __align__(128) uint8_t smem[];
+  fwht_phase<K, false>(X, T, chan_max_bits, Xr, smem);
+  const int tid = threadIdx.x;
+  const int rr = tid / TPR, j0 = (tid % TPR) * 32;
+  int pj[32];
+  load_perm32(perm, j0, pj);  // an offline input: these loads overlap the grid barrier
+
+  // ---- grid barrier (X~ stores -- read back below by TMA, i.e. the async proxy -- and chan_max atomics
+  // visible everywhere): every thread fences, the cluster synchronises, one thread per cluster counts in
+  // and waits for all clusters, then releases its cluster
+  trace(1, 0);
+  __threadfence();
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  ptx::cluster_sync();
+  if (ptx::cluster_ctarank() == 0 && threadIdx.x == 0) {
+    atomicAdd(counter, 1u);
+    const unsigned nclusters = gridDim.x / kColmaxCluster;
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      if (v >= nclusters) break;
+      __nanosleep(64);
+    }
+  }
+  ptx::cluster_sync();
+  trace(1, 1);
+
+  // ---- quantisation pass (a3-a6) on this CTA's rows
+  float* stage = reinterpret_cast<float*>(smem);                                   // 2 f32 row tiles
+  float* cms = reinterpret_cast<float*>(smem + S::TILE_D);                         // chan_max [K]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::TILE_D + 2 * S::STAGE) + 2;  // 3 fresh barriers
+  float* red = reinterpret_cast<float*>(smem + S::TILE_D + 2 * S::STAGE + 64);
+  const int64_t ntiles = (T + P::R - 1) / P::R;
+  auto issue = [&](int64_t tile, int buf) {
+    const int64_t rows = (T - tile * P::R) < P::R ? (T - tile * P::R) : P::R;
+    const uint32_t bytes = (uint32_t)(rows * K * 4);
+    ptx::mbar_arrive_expect_tx(&bar[buf], bytes);
+    ptx::bulk_load(stage + buf * P::TILE, Xr + tile * P::R * K, bytes, &bar[buf]);
+  };
+  if (tid == 0) {
+    // chan_max -> every CTA of the cluster: each rank fetches one eighth once from L2 and multicasts it
+    ptx::mbar_arrive_expect_tx(&bar[2], K * 4);
+    const uint32_t rank = ptx::cluster_ctarank();
+    constexpr int SL = K / kColmaxCluster;
+    ptx::bulk_load_multicast(cms + rank * SL, chan_max_bits + rank * SL, SL * 4, &bar[2],
+                             (uint16_t)((1u << kColmaxCluster) - 1));
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  }
+  trace(1, 2);
+  ptx::mbar_wait(&bar[2], 0);
+  trace(1, 4);
+  const float inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out);
+  trace(1, 5);
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    ptx::mbar_wait(&bar[buf], (it >> 1) & 1);  // bar[0], bar[1] of this pass (fresh: phase 0 first)
+    trace(1, 6 + (it < 8 ? it : 8));
+    quant_row<TPR>(stage + buf * P::TILE + rr * K, pj, inv_s, true, red, tid, rr, tile * P::R + rr, T, K, j0, Xq, Xq8,
+                   scale_out, e4m3 != 0, [&] {
+                     if (tid == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
+                   });
+  }
+  trace(1, 15);
+  ptx::pdl_launch_dependents();
 }
 
 template <int K>
@@ -199,14 +406,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
   }
   trace(1, 0);
   int pj[32];  // perm is an offline input: read it before waiting for the FWHT pass
-  {
-    const int4* pp = reinterpret_cast<const int4*>(perm + j0);
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int4 w = __ldg(pp + q);
-      pj[4 * q] = w.x; pj[4 * q + 1] = w.y; pj[4 * q + 2] = w.z; pj[4 * q + 3] = w.w;
-    }
-  }
+  load_perm32(perm, j0, pj);
   ptx::pdl_wait();  // X~ and chan_max come from fwht_colmax_kernel
   __syncthreads();
   trace(1, 1);
@@ -216,18 +416,10 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
   }
   float inv_s = 1.0f;
   if (smooth) {
-    // chan_max -> shared memory (coalesced), then s_g = max_{j' in g} c[perm[j']]  (4 consecutive
-    // threads cover one 128-wide group)
-    for (int c = tid * 4; c < K; c += Q::THREADS * 4)
+    for (int c = tid * 4; c < K; c += Q::THREADS * 4)  // chan_max -> shared memory, coalesced
       *reinterpret_cast<uint4*>(cms + c) = __ldcg(reinterpret_cast<const uint4*>(chan_max_bits + c));
     __syncthreads();
-    float m = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) m = fmaxf(m, cms[pj[k]]);
-    m = seg_max(m, 4);
-    if (m == 0.0f) m = 1.0f;  // R8: zero group -> scale 1
-    inv_s = __frcp_rn(m);     // R9: fl(1/s_g)
-    if (blockIdx.x == 0 && rr == 0 && (j0 & 127) == 0 && s_group_out) s_group_out[j0 >> 7] = m;
+    inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out);
   }
   trace(1, 2);
 
@@ -236,79 +428,11 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
     const int buf = it % STAGES;
     ptx::mbar_wait(&bar[buf], (it / STAGES) & 1);
     trace(1, 3 + (it < 10 ? it : 10));
-    const float* xs = stage + buf * Q::TILE + rr * K;
-    float z[32];
-    float m = 0.0f;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const float x = xs[pj[k]];
-      z[k] = smooth ? __fmul_rn(x, inv_s) : x;
-      m = fmaxf(m, fabsf(z[k]));
-    }
-    // per-token absmax over the TPR threads of this row
-    if constexpr (TPR <= 32) {
-      m = seg_max(m, TPR);
-    } else {
-      m = seg_max(m, 32);
-      if ((tid & 31) == 0) red[tid >> 5] = m;
-      __syncthreads();
-      const int w0 = (rr * TPR) >> 5;
-      float mm = 0.0f;
-#pragma unroll 4
-      for (int w = 0; w < TPR / 32; ++w) mm = fmaxf(mm, red[w0 + w]);
-      m = mm;
-    }
-    __syncthreads();  // every thread has read stage[buf] (and red): both may be reused
-    if (tid == 0 && tile + STAGES * (int64_t)gridDim.x < ntiles) issue(tile + STAGES * (int64_t)gridDim.x, buf);
-    const int64_t trow = tile * Q::R + rr;
-    if (trow < T) {
-      float alpha = 1.0f, r = 0.0f;
-      if (m > 0.0f) {
-        alpha = __fdiv_rn(m, 7.0f);  // stored scale alpha_t = fl(m/7)
-        r = __fdiv_rn(7.0f, m);      // R9: codes use fl(7/m)
-      }
-      if (Xq == nullptr && e4m3) {
-        // hot path (rrs_linear): only the E4M3 operand.  rint (RNE) then clamp in f32 -- the same integer
-        // as __float2int_rn + clamp -- and one cvt per pair (integers of magnitude <= 8 are exact in E4M3).
-        uint32_t w[8];
-#pragma unroll
-        for (int k = 0; k < 32; k += 4) {
-          float q[4];
-#pragma unroll
-          for (int h = 0; h < 4; ++h)  // R10, R11; "+ 0" turns rint's -0 into the canonical +0 (code byte 0x00)
-            q[h] = __fadd_rn(fminf(fmaxf(rintf(__fmul_rn(z[k + h], r)), -8.0f), 7.0f), 0.0f);
-          uint32_t lo, hi;
-          asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
-              : "=r"(lo) : "f"(q[1]), "f"(q[0]));
-          asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
-              : "=r"(hi) : "f"(q[3]), "f"(q[2]));
-          w[k >> 2] = lo | (hi << 16);
-        }
-        uint4* dst = reinterpret_cast<uint4*>(Xq8 + trow * K + j0);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-      } else {
-        uint32_t packed[4] = {0u, 0u, 0u, 0u};
-        uint32_t wide[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
-#pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          int q = __float2int_rn(__fmul_rn(z[k], r));  // R10: round half to even
-          q = max(-8, min(7, q));                      // R11
-          packed[k >> 3] |= (uint32_t)(q & 0xF) << ((k & 7) * 4);
-          wide[k >> 2] |= operand_byte(q, e4m3 != 0) << ((k & 3) * 8);
-        }
-        if (Xq) {
-          *reinterpret_cast<uint4*>(Xq + trow * (K / 2) + j0 / 2) =
-              make_uint4(packed[0], packed[1], packed[2], packed[3]);
-        }
-        if (Xq8) {
-          uint4* dst = reinterpret_cast<uint4*>(Xq8 + trow * K + j0);
-          dst[0] = make_uint4(wide[0], wide[1], wide[2], wide[3]);
-          dst[1] = make_uint4(wide[4], wide[5], wide[6], wide[7]);
-        }
-      }
-      if (j0 == 0) scale_out[trow] = alpha;
-    }
+    quant_row<TPR>(stage + buf * Q::TILE + rr * K, pj, inv_s, smooth, red, tid, rr, tile * Q::R + rr, T, K, j0, Xq,
+                   Xq8, scale_out, e4m3 != 0, [&] {
+                     if (tid == 0 && tile + STAGES * (int64_t)gridDim.x < ntiles)
+                       issue(tile + STAGES * (int64_t)gridDim.x, buf);
+                   });
   }
   trace(1, 15);
   ptx::pdl_launch_dependents();
@@ -368,6 +492,33 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
 }
 
 template <int K>
+static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, float* Xr, unsigned* counter,
+                                  const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3,
+                                  int nsm, cudaStream_t st) {
+  using P = FwhtPlan<K>;
+  auto kern = prologue_fused_kernel<K>;
+  const int smem = ColmaxSmem<K>::BYTES;
+  cudaError_t e = prepare_kernel(kern, smem, P::THREADS);
+  if (e != cudaSuccess) return e;
+  // every CTA must be resident at once (grid barrier): the grid is exactly the co-resident cluster count
+  static int max_clusters = 0;
+  if (max_clusters == 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kColmaxCluster * 1024);
+    cfg.blockDim = dim3(P::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) return cudaErrorInvalidConfiguration;
+    max_clusters = n;
+  }
+  const int64_t tiles = (T + P::R - 1) / P::R;
+  const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + kColmaxCluster - 1) / kColmaxCluster));
+  const int grid = (int)clusters * kColmaxCluster;
+  kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr, counter, perm, s_group, Xq, Xq8, scale, (int)e4m3);
+  return cudaGetLastError();
+}
+
+template <int K>
 static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* perm, const unsigned* cm,
                                   float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int nsm,
                                   cudaStream_t st) {
@@ -385,6 +536,21 @@ static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* per
 }
 
 #define RRS_FOR_EACH_K(M) M(128) M(256) M(512) M(1024) M(2048) M(4096) M(8192) M(16384) M(7168) M(14336)
+
+#define RRS_FOR_EACH_POW2_K(M) M(128) M(256) M(512) M(1024) M(2048) M(4096) M(8192) M(16384)
+
+bool prologue_fused_supports_k(int64_t K) { return K >= 128 && K <= 16384 && (K & (K - 1)) == 0; }
+
+cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
+                                  unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,
+                                  float* scale, bool e4m3, int nsm, cudaStream_t st) {
+  switch (K) {
+#define RRS_CASE(k) case k: return launch_fused_k<k>(X, T, chan_max_bits, Xr, counter, perm, s_group, Xq, Xq8, scale, e4m3, nsm, st);
+    RRS_FOR_EACH_POW2_K(RRS_CASE)
+#undef RRS_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 bool prologue_supports_k(int64_t K) {
   switch (K) {

@@ -58,10 +58,12 @@ RRS_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 // 32-bit load from the shared memory of CTA `rank` of this cluster at the address of local `p`
+// (not volatile, no memory clobber: independent loads may be issued back to back; callers order them
+// against peer writes with cluster barriers)
 RRS_DEV uint32_t ld_dsmem_u32(const void* p, uint32_t rank) {
   uint32_t remote, v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote) : "memory");
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
   return v;
 }
 // programmatic dependent launch: wait for the preceding grid's memory; allow the next grid to launch
@@ -123,6 +125,16 @@ RRS_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, uint32_t bar_clu
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(bar_cluster_addr), "l"(cache_hint)
+      : "memory");
+}
+// 1-D bulk copy global -> the same shared offset in every CTA of cta_mask (cluster multicast); each
+// destination CTA's mbarrier (same offset) receives the complete_tx of its copy.
+RRS_DEV void bulk_load_multicast(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,
+                                 uint16_t cta_mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(gmem_src)), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
       : "memory");
 }
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
