@@ -28,6 +28,7 @@
 // The MMA of group g+1 overlaps the promotion of group g (two TMEM buffers).  In plain mode (the
 // per-channel A4W4 baseline of P:322) the MMA accumulates all K into one buffer per tile instead.
 #include <algorithm>
+#include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
@@ -69,8 +70,10 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK;                  // 16 KiB
   static constexpr int B_BYTES = B_ROWS * BK;              // 30 / 15 KiB (whole 8-row swizzle atoms)
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = kCta == 1 ? 4 : 6;
-  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + 1024 /*barriers*/ +
+  static constexpr int STAGES = kCta == 1 ? 3 : 5;
+  static constexpr int EPI_TILE_BYTES = 32 * EPI_COLS * 2;  // one promotion warp's bf16 Y sub-tile (TMA store)
+  static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + NUM_EPI_WARPS * EPI_TILE_BYTES +
+                                    1024 /*barriers*/ +
                                     MAX_G * 4 + BN * 4 + 64;
   static_assert(B_ROWS % 8 == 0 && (STAGES * A_BYTES) % 1024 == 0 && B_BYTES % 1024 == 0, "swizzle atoms");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
@@ -87,12 +90,13 @@ struct GemmParams {
   void* Y;
   int64_t ldy;
   int32_t* P_debug;
+  int y_tma;  // bf16 Y written by TMA tensor stores (16-byte aligned base, ldy % 8 == 0)
 };
 
 template <bool kPlain, bool kF32Out, bool kDebug, int kCta, bool kFp8>
 __global__ void __launch_bounds__(gemm::THREADS, 1)
 rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
-                GemmParams p) {
+                const __grid_constant__ CUtensorMap tmap_y, GemmParams p) {
   using namespace gemm;
   using C = Cfg<kCta>;
   constexpr int STAGES = C::STAGES, A_BYTES = C::A_BYTES, B_BYTES = C::B_BYTES, STAGE_BYTES = C::STAGE_BYTES;
@@ -102,12 +106,13 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint8_t* sY = smem + STAGES * STAGE_BYTES;  // [NUM_EPI_WARPS][32 rows][EPI_COLS] bf16 output staging
+  uint64_t* full = reinterpret_cast<uint64_t*>(sY + NUM_EPI_WARPS * C::EPI_TILE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;   // [2]
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  float* s_sm = reinterpret_cast<float*>(smem + STAGES * STAGE_BYTES + 1024);
+  float* s_sm = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
   float* beta_sm = s_sm + MAX_G;
   uint32_t* bias_sm = reinterpret_cast<uint32_t*>(beta_sm + BN);  // [8] = 0x4B400000
 
@@ -119,6 +124,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmap_x);
     ptx::prefetch_tmap(&tmap_w);
+    if constexpr (!kF32Out && !kDebug) ptx::prefetch_tmap(&tmap_y);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
@@ -369,9 +375,9 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
       if (threadIdx.x - 64 < BN) beta_sm[threadIdx.x - 64] = beta_pref;
       asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
-      if (p.Y != nullptr && row < p.T) {
+      if (p.Y != nullptr && (row < p.T || (!kF32Out && !kDebug && p.y_tma))) {
         const float rs = xs_pref * p.out_scale;
-        if constexpr (kF32Out) {
+        if constexpr (kF32Out || kDebug) {
           float* yrow = reinterpret_cast<float*>(p.Y) + (int64_t)row * p.ldy;
 #pragma unroll
           for (int c = 0; c < EPI_COLS; c += 4) {
@@ -389,7 +395,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
               if (n + 2 < p.N) yrow[n + 2] = v.z;
             }
           }
-        } else {
+        } else if (!p.y_tma) {
           __nv_bfloat16* yrow = reinterpret_cast<__nv_bfloat16*>(p.Y) + (int64_t)row * p.ldy;
 #pragma unroll
           for (int c = 0; c < EPI_COLS; c += 8) {
@@ -410,10 +416,37 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
                 if (n + h < p.N) yrow[n + h] = e[h];
             }
           }
+        } else {
+          // bf16: this warp's 32 x 80 sub-tile goes through shared memory and one TMA tensor store (coalesced,
+          // asynchronous, clipped at the T / N edges by the tensor map) instead of 32-row scattered stores
+          uint8_t* my = sY + ew * C::EPI_TILE_BYTES;
+          if (lane == 0) ptx::bulk_wait_group_read0();  // the previous tile's store has read this buffer
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < EPI_COLS; c += 8) {
+            uint32_t w[4];
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+              const float a0 = (acc[c + 2 * h] * rs) * beta_sm[half * EPI_COLS + c + 2 * h];
+              const float a1 = (acc[c + 2 * h + 1] * rs) * beta_sm[half * EPI_COLS + c + 2 * h + 1];
+              const __nv_bfloat162 bb = __floats2bfloat162_rn(a0, a1);
+              w[h] = *reinterpret_cast<const uint32_t*>(&bb);
+            }
+            *reinterpret_cast<uint4*>(my + lane * (EPI_COLS * 2) + c * 2) = make_uint4(w[0], w[1], w[2], w[3]);
+          }
+          ptx::fence_proxy_async_shared();
+          __syncwarp();
+          if (lane == 0) {
+            ptx::tma_store_2d(&tmap_y, my, col0, m_blk * BM * kCta + (int)rank * BM + quad * 32);
+            ptx::bulk_commit_group();
+          }
         }
       }
       if (trace_epi) gtrace(15, 7);
     }
+  }
+  if constexpr (!kF32Out && !kDebug) {
+    if (p.y_tma && warp >= 2 && lane == 0) ptx::bulk_wait_group0();  // Y stores complete before the CTA retires
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -452,8 +485,23 @@ static bool make_tmap(CUtensorMap* m, const void* base, int64_t rows, int64_t K,
   return r == CUDA_SUCCESS;
 }
 
+// 2-D bf16 row-major Y [T][ldy] (N valid columns), written in (32 rows x EPI_COLS) boxes; the map clips the
+// T / N edges so ragged tiles need no masking
+static bool make_tmap_y(CUtensorMap* m, void* base, int64_t T, int64_t N, int64_t ldy) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)T};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldy * 2)};
+  cuuint32_t box[2] = {(cuuint32_t)gemm::EPI_COLS, 32u};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <bool kPlain, bool kF32, bool kDebug, int kCta, bool kFp8>
-static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, const GemmParams& p, int grid,
+static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
+                                  const GemmParams& p, int grid,
                                   cudaStream_t st) {
   auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug, kCta, kFp8>;
   constexpr int smem = gemm::Cfg<kCta>::SMEM_BYTES;
@@ -473,7 +521,7 @@ static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, 
   attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kern, tx, tw, p);
+  return cudaLaunchKernelEx(&cfg, kern, tx, tw, ty, p);
 }
 
 template <int kCta, bool kFp8>
@@ -497,14 +545,20 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.Y = a.Y;
   p.ldy = a.ldy;
   p.P_debug = a.P_debug;
+  // bf16 output tile stores through TMA when the layout allows it (else per-thread 16-byte stores)
+  CUtensorMap ty;
+  memset(&ty, 0, sizeof(ty));
+  p.y_tma = 0;
+  if (a.Y && a.y_dtype != 1 && !a.P_debug && a.ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0)
+    p.y_tma = make_tmap_y(&ty, a.Y, a.T, a.N, a.ldy) ? 1 : 0;
   const int grid = std::min(p.num_tiles, nsm / kCta) * kCta;
   const bool f32 = a.y_dtype == 1;
-  if (a.P_debug) return launch_variant<false, true, true, kCta, kFp8>(tx, tw, p, grid, st);
+  if (a.P_debug) return launch_variant<false, true, true, kCta, kFp8>(tx, tw, ty, p, grid, st);
   if (a.plain)
-    return f32 ? launch_variant<true, true, false, kCta, kFp8>(tx, tw, p, grid, st)
-               : launch_variant<true, false, false, kCta, kFp8>(tx, tw, p, grid, st);
-  return f32 ? launch_variant<false, true, false, kCta, kFp8>(tx, tw, p, grid, st)
-             : launch_variant<false, false, false, kCta, kFp8>(tx, tw, p, grid, st);
+    return f32 ? launch_variant<true, true, false, kCta, kFp8>(tx, tw, ty, p, grid, st)
+               : launch_variant<true, false, false, kCta, kFp8>(tx, tw, ty, p, grid, st);
+  return f32 ? launch_variant<false, true, false, kCta, kFp8>(tx, tw, ty, p, grid, st)
+             : launch_variant<false, false, false, kCta, kFp8>(tx, tw, ty, p, grid, st);
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {
