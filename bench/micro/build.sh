@@ -12,3 +12,5 @@ nvcc $ARCH -O3 -std=c++17 -DRRS_TRACE -I../../include -I$NI -o gemm_trace gemm_t
   -lcuda -L$NL -l:libnccl.so.2 -Xlinker -rpath=$NL
 nvcc $ARCH -O3 -std=c++17 -DRRS_TRACE -I../../include -I$NI -o prologue_trace prologue_trace.cu $C/api.cu $C/gemm.cu \
   -lcuda -L$NL -l:libnccl.so.2 -Xlinker -rpath=$NL
+nvcc $ARCH -O3 -std=c++17 -I../../include -I$NI -o gemm_time gemm_time.cu $C/api.cu $C/prologue.cu \
+  -lcuda -L$NL -l:libnccl.so.2 -Xlinker -rpath=$NL

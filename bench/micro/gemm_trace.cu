@@ -1,4 +1,4 @@
-// Timeline of the RRS GEMM's MMA / promotion handshake (first tile, first 16 groups, per CTA).
+// Timeline of the RRS GEMM's MMA / promotion handshake per CTA: first tile, tile boundary, second tile.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DRRS_TRACE -I../../include -o gemm_trace
 //        gemm_trace.cu -lcuda
 #include <cstdio>
@@ -32,17 +32,24 @@ int main(int argc, char** argv) {
     printf("rep %d: %s/%s %.1f us = %.0f TOPS\n", rep, cudaGetErrorString(err), cudaGetErrorString(e2), ms * 1e3,
            2.0 * T * N * K / (ms * 1e-3) / 1e12);
   }
-  static unsigned long long h[160][16][8];
+  static unsigned long long h[160][32][8];
   cudaMemcpyFromSymbol(h, rrs::g_gtrace, sizeof(h));
-  for (int c : {0, 1, 2, 3, 100, 101}) {
+  const int G = (int)(K / 128);
+  for (int c : {0, 1, 2, 100}) {
     unsigned long long t0 = h[c][0][0] ? h[c][0][0] : h[c][0][3];
-    printf("CTA %d (ns from its first MMA wait):\n  g : tempty  full  issued | w0 tfull  w0 rel | wl tfull  wl rel\n", c);
-    for (int g = 0; g < 16; ++g) {
-      auto f = [&](int s) { return h[c][g][s] ? (long long)(h[c][g][s] - t0) : -1LL; };
-      printf("  %2d: %6lld %6lld %6lld | %6lld %6lld | %6lld %6lld\n", g, f(0), f(1), f(2), f(3), f(4), f(5), f(6));
+    printf("CTA %d (ns from its first MMA wait):\n  tile g : tempty  full  issued | w0 tfull  w0 rel | wl tfull  wl rel\n", c);
+    for (int r = 0; r < 32; ++r) {
+      const int it = r < 24 ? 0 : 1, g = r < 16 ? r : (r < 24 ? G - 8 + (r - 16) : r - 24);
+      if (r == 16 && G <= 16) continue;
+      auto f = [&](int s) { return h[c][r][s] ? (long long)(h[c][r][s] - t0) : -1LL; };
+      printf("  %d %3d: %6lld %6lld %6lld | %6lld %6lld | %6lld %6lld\n", it, g, f(0), f(1), f(2), f(3), f(4), f(5), f(6));
     }
-    if (h[c][14][7]) printf("  first tile epilogue: %lld -> %lld ns (%lld ns)\n", (long long)(h[c][14][7] - t0),
-                            (long long)(h[c][15][7] - t0), (long long)(h[c][15][7] - h[c][14][7]));
+    const char* lab[8] = {"epi start", "beta staged", "store buf free", "staged", "store issued", "epi end",
+                          "tile start (acc zeroed)", "-"};
+    for (int it = 0; it < 2; ++it)
+      for (int k = 0; k < 7; ++k)
+        if (h[c][8 * it + k][7])
+          printf("  tile %d %-24s %lld\n", it, lab[k], (long long)(h[c][8 * it + k][7] - t0));
   }
   return 0;
 }

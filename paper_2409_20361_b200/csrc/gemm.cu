@@ -39,18 +39,26 @@
 namespace rrs {
 
 // Optional timeline (bench/micro/gemm_trace.cu builds this file with -DRRS_TRACE): %globaltimer at fixed
-// points of the first tile's first 16 groups, per CTA: [0] MMA after tempty wait, [1] after full wait,
-// [2] after issue; [3]/[4] first promotion warp after tfull wait / after release; [5]/[6] last warp.
+// points, per CTA, of the first tile's first 16 groups (rows 0..15), the first tile's last 8 groups
+// (rows 16..23) and the second tile's first 8 groups (rows 24..31): [0] MMA after tempty wait, [1] after
+// full wait, [2] after issue; [3]/[4] first promotion warp after tfull wait / after release; [5]/[6] last
+// warp; [7] of rows 0/1 (tile 0) and 2/3 (tile 1): epilogue start / store issued.
 #ifdef RRS_TRACE
-__device__ unsigned long long g_gtrace[160][16][8];
-__device__ __forceinline__ void gtrace(int g, int slot) {
-  if (blockIdx.x < 160 && g < 16) {
+__device__ unsigned long long g_gtrace[160][32][8];
+__device__ __forceinline__ int gtrace_row(int it, int g, int G) {
+  if (it == 0) return g < 16 ? g : (g >= G - 8 ? 16 + g - (G - 8) : -1);
+  if (it == 1) return g < 8 ? 24 + g : -1;
+  return -1;
+}
+__device__ __forceinline__ void gtrace(int row, int slot) {
+  if (blockIdx.x < 160 && row >= 0 && row < 32) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    g_gtrace[blockIdx.x][g][slot] = t;
+    g_gtrace[blockIdx.x][row][slot] = t;
   }
 }
 #else
+__device__ __forceinline__ int gtrace_row(int, int, int) { return -1; }
 __device__ __forceinline__ void gtrace(int, int) {}
 #endif
 
@@ -74,7 +82,7 @@ struct Cfg {
   static constexpr int EPI_TILE_BYTES = 32 * EPI_COLS * 2;  // one promotion warp's bf16 Y sub-tile (TMA store)
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + NUM_EPI_WARPS * EPI_TILE_BYTES +
                                     1024 /*barriers*/ +
-                                    MAX_G * 4 + BN * 4 + 64;
+                                    MAX_G * 4 + 2 * BN * 4 + 2 * BM * 4 + 64;
   static_assert(B_ROWS % 8 == 0 && (STAGES * A_BYTES) % 1024 == 0 && B_BYTES % 1024 == 0, "swizzle atoms");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
@@ -113,8 +121,9 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   uint64_t* tempty = tfull + 2;       // [2]
   uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* s_sm = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
-  float* beta_sm = s_sm + MAX_G;
-  uint32_t* bias_sm = reinterpret_cast<uint32_t*>(beta_sm + BN);  // [8] = 0x4B400000
+  float* beta_sm = s_sm + MAX_G;     // [2][BN]   beta of the current tile (double-buffered by tile parity)
+  float* xs_sm = beta_sm + 2 * BN;   // [2][BM]   alpha_t of the current / next tile's rows
+  uint32_t* bias_sm = reinterpret_cast<uint32_t*>(xs_sm + 2 * BM);  // [8] = 0x4B400000
 
   const uint32_t warp = ptx::warp_idx();
   const int lane = threadIdx.x & 31;
@@ -182,9 +191,11 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     int stage = 0;
     uint32_t phase = 0;
     uint32_t acc_iter = 0;  // number of accumulator buffers filled so far
+    int it = 0;             // local tile counter (timeline only)
     const uint64_t a_desc0 = ptx::smem_desc_sw128(sA), b_desc0 = ptx::smem_desc_sw128(sB);
     for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
-      for (int kb = 0; kb < p.G; ++kb) {
+      for (int kb = 0; kb < p.G; ++kb, it += (kb == p.G)) {
+        const int trow = gtrace_row(it, kb, p.G);
         const uint32_t b = acc_iter & 1;
         if (kPlain ? kb == 0 : true) {
           // use u = acc_iter >> 1 of buffer b needs the (u)-th release (completion #u of tempty[b]); the
@@ -192,9 +203,9 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
           else ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
         }
-        if (tile == (int)blockIdx.x / kCta) gtrace(kb, 0);
+        gtrace(trow, 0);
         ptx::mbar_wait_spin(&full[stage], phase);
-        if (tile == (int)blockIdx.x / kCta) gtrace(kb, 1);
+        gtrace(trow, 1);
         ptx::tc_fence_after();
         // descriptor start addresses advance in 16-byte units: stage offsets, then 32 bytes per K step
         const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
@@ -220,7 +231,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           ptx::mma_commit_pair(&empty[stage], 0x3);
           if (!kPlain || kb == p.G - 1) ptx::mma_commit_pair(&tfull[b], 0x3);
         }
-        if (tile == (int)blockIdx.x / kCta) gtrace(kb, 2);
+        gtrace(trow, 2);
         if (!kPlain || kb == p.G - 1) ++acc_iter;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
@@ -264,23 +275,42 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
 #pragma unroll
     for (int j = 0; j < 8; ++j) bias8[j] = bias_sm[j];
     uint32_t acc_iter = 0;
-    for (int tile = blockIdx.x / kCta; tile < p.num_tiles; tile += gridDim.x / kCta) {
+    int it = 0;  // local tile counter
+    const int tile_stride = gridDim.x / kCta;
+    const int et = (int)threadIdx.x - 64;  // 0 .. 383: epilogue thread index
+    // alpha_t (per row) and beta_n (per column) reach shared memory through cp.async, never through
+    // registers: alpha one tile ahead (it is folded into every group's scale), beta during the tile's K loop.
+    // Completion: cp.async.wait_group 0 + the epilogue's named barrier.
+    auto fetch_xs = [&](int tile, int buf) {
+      if (et < BM) {
+        const int r = (tile % p.num_m) * BM * kCta + (int)rank * BM + et;
+        const bool ok = tile < p.num_tiles && p.x_scale && r < p.T;
+        ptx::cp_async4(xs_sm + buf * BM + et, ok ? p.x_scale + r : p.x_scale, ok ? 4u : 0u);
+      }
+    };
+    fetch_xs(blockIdx.x / kCta, 0);
+    ptx::cp_async_commit();
+    ptx::cp_async_wait_all();
+    asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
+    for (int tile = blockIdx.x / kCta; tile < p.num_tiles; tile += tile_stride, ++it) {
       const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
       const int row = m_blk * BM * kCta + (int)rank * BM + row_in_tile;
       const int col0 = n_blk * BN + half * EPI_COLS;
-      // the epilogue's scales are loaded now and only consumed after the last group, so their global-memory
-      // latency is hidden behind the whole K loop
-      float beta_pref = 0.0f, xs_pref = 0.0f;
-      {
-        const int c = threadIdx.x - 64;
-        const int n = n_blk * BN + c;
-        if (p.w_scale && c < BN && n < p.N) beta_pref = __ldg(p.w_scale + n);
-        if (p.x_scale && row < p.T) xs_pref = __ldg(p.x_scale + row);
+      // rs = alpha_t * out_scale is folded into every group's scale (acc = sum_g fl(s_g * rs) * P_g), so the
+      // epilogue is a single multiply by beta_n
+      const float rs = xs_sm[(it & 1) * BM + row_in_tile] * p.out_scale;
+      if (et < BN) {
+        const int n = n_blk * BN + et;
+        const bool ok = p.w_scale && n < p.N;
+        ptx::cp_async4(beta_sm + (it & 1) * BN + et, ok ? p.w_scale + n : p.w_scale, ok ? 4u : 0u);
       }
+      fetch_xs(tile + tile_stride, (it + 1) & 1);
+      ptx::cp_async_commit();
 
       float2 acc2[EPI_COLS / 2];  // acc pairs (columns 2i, 2i+1 of this thread's EPI_COLS)
 #pragma unroll
       for (int c = 0; c < EPI_COLS / 2; ++c) acc2[c] = make_float2(0.0f, 0.0f);
+      if (it < 2 && lane == 0 && ew == 0) gtrace(8 * it + 6, 7);
       const int ngroups = kPlain ? 1 : p.G;
       for (int g = 0; g < ngroups; ++g) {
         const uint32_t b = acc_iter & 1;
@@ -288,11 +318,20 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         if constexpr (kPlain) ptx::mbar_wait(&tfull[b], (acc_iter >> 1) & 1);
         else ptx::mbar_wait_spin(&tfull[b], (acc_iter >> 1) & 1);
         ptx::tc_fence_after();
-        const bool trace_me = tile == (int)blockIdx.x / kCta && lane == 0 && (ew == 0 || ew == NUM_EPI_WARPS - 1);
-        if (trace_me) gtrace(g, ew == 0 ? 3 : 5);
-        const float s = kPlain ? 1.0f : s_sm[g];
+        const bool trace_me = lane == 0 && (ew == 0 || ew == NUM_EPI_WARPS - 1);
+        const int trow = gtrace_row(it, g, p.G);
+        if (trace_me) gtrace(trow, ew == 0 ? 3 : 5);
+        const float s = kPlain ? rs : s_sm[g] * rs;
         const float2 s2 = make_float2(s, s);
         const uint32_t tbase = tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS;
+#if defined(RRS_TRACE) && defined(RRS_GEXP) && RRS_GEXP == 1
+        if constexpr (kFp8 && !kDebug) {  // timeline experiment: no TMEM readout at all
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+          acc2[g % (EPI_COLS / 2)].x += s;
+        } else
+#endif
         if constexpr (kFp8 && !kDebug) {
           // software-pipelined: chunk c+1 is in flight while chunk c is accumulated; the buffer is released
           // as soon as the last chunk has landed in registers
@@ -305,6 +344,10 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             uint32_t(&cur)[16] = (cc & 1) ? rb : ra;
             uint32_t(&nxt)[16] = (cc & 1) ? ra : rb;
             if (cc + 1 < NCH) RRS_TMEM_LD16(tbase + (cc + 1) * 16, nxt);
+#if defined(RRS_TRACE) && defined(RRS_GEXP) && RRS_GEXP == 2
+            for (int j = 0; j < 8; ++j) acc2[cc * 8 + j].x = __uint_as_float(__float_as_uint(acc2[cc * 8 + j].x) ^ cur[2 * j] ^ cur[2 * j + 1]);
+            if (false)
+#endif
 #pragma unroll
             for (int j = 0; j < 8; ++j)  // acc += s_g * P_g (R14); the FP8 carrier's P_g is an exact float
               acc2[cc * 8 + j] = __ffma2_rn(s2, make_float2(__uint_as_float(cur[2 * j]), __uint_as_float(cur[2 * j + 1])),
@@ -315,7 +358,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
-                if (trace_me) gtrace(g, ew == 0 ? 4 : 6);
+                if (trace_me) gtrace(trow, ew == 0 ? 4 : 6);
               }
             }
           }
@@ -362,87 +405,79 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         }
         ++acc_iter;
       }
-      float acc[EPI_COLS];
-#pragma unroll
-      for (int c = 0; c < EPI_COLS / 2; ++c) {
-        acc[2 * c] = acc2[c].x;
-        acc[2 * c + 1] = acc2[c].y;
-      }
-      // ---- epilogue: Y = acc * (alpha_t * out_scale) * beta_n
-      const bool trace_epi = tile == (int)blockIdx.x / kCta && lane == 0 && ew == 0;
-      if (trace_epi) gtrace(14, 7);
-      // stage this tile's beta (named barrier among the epilogue threads: the previous tile's readers are done)
+      // ---- epilogue: Y = acc * beta_n  (acc already carries alpha_t * out_scale)
+      const bool trace_epi = it < 2 && lane == 0 && ew == 0;
+      if (trace_epi) gtrace(8 * it, 7);
+      // this tile's beta and the next tile's alpha have landed (every thread's copies: wait + named barrier);
+      // the buffers written next were last read before this barrier
+      ptx::cp_async_wait_all();
       asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
-      if (threadIdx.x - 64 < BN) beta_sm[threadIdx.x - 64] = beta_pref;
-      asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
+      if (trace_epi) gtrace(8 * it + 1, 7);
+      const float2* beta2 = reinterpret_cast<const float2*>(beta_sm + (it & 1) * BN + half * EPI_COLS);
       if (p.Y != nullptr && (row < p.T || (!kF32Out && !kDebug && p.y_tma))) {
-        const float rs = xs_pref * p.out_scale;
         if constexpr (kF32Out || kDebug) {
           float* yrow = reinterpret_cast<float*>(p.Y) + (int64_t)row * p.ldy;
 #pragma unroll
           for (int c = 0; c < EPI_COLS; c += 4) {
             const int n = col0 + c;
-            float4 v;
-            v.x = (acc[c] * rs) * beta_sm[half * EPI_COLS + c];
-            v.y = (acc[c + 1] * rs) * beta_sm[half * EPI_COLS + c + 1];
-            v.z = (acc[c + 2] * rs) * beta_sm[half * EPI_COLS + c + 2];
-            v.w = (acc[c + 3] * rs) * beta_sm[half * EPI_COLS + c + 3];
+            const float2 lo = __fmul2_rn(acc2[c / 2], beta2[c / 2]), hi = __fmul2_rn(acc2[c / 2 + 1], beta2[c / 2 + 1]);
             if (n + 3 < p.N) {
-              *reinterpret_cast<float4*>(yrow + n) = v;
+              *reinterpret_cast<float4*>(yrow + n) = make_float4(lo.x, lo.y, hi.x, hi.y);
             } else {
-              if (n < p.N) yrow[n] = v.x;
-              if (n + 1 < p.N) yrow[n + 1] = v.y;
-              if (n + 2 < p.N) yrow[n + 2] = v.z;
-            }
-          }
-        } else if (!p.y_tma) {
-          __nv_bfloat16* yrow = reinterpret_cast<__nv_bfloat16*>(p.Y) + (int64_t)row * p.ldy;
-#pragma unroll
-          for (int c = 0; c < EPI_COLS; c += 8) {
-            const int n = col0 + c;
-            uint32_t w[4];
-#pragma unroll
-            for (int h = 0; h < 4; ++h) {
-              const float a0 = (acc[c + 2 * h] * rs) * beta_sm[half * EPI_COLS + c + 2 * h];
-              const float a1 = (acc[c + 2 * h + 1] * rs) * beta_sm[half * EPI_COLS + c + 2 * h + 1];
-              const __nv_bfloat162 bb = __floats2bfloat162_rn(a0, a1);
-              w[h] = *reinterpret_cast<const uint32_t*>(&bb);
-            }
-            if (n + 7 < p.N) {
-              *reinterpret_cast<uint4*>(yrow + n) = make_uint4(w[0], w[1], w[2], w[3]);
-            } else {
-              const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(w);
-              for (int h = 0; h < 8; ++h)
-                if (n + h < p.N) yrow[n + h] = e[h];
+              if (n < p.N) yrow[n] = lo.x;
+              if (n + 1 < p.N) yrow[n + 1] = lo.y;
+              if (n + 2 < p.N) yrow[n + 2] = hi.x;
             }
           }
         } else {
-          // bf16: this warp's 32 x 80 sub-tile goes through shared memory and one TMA tensor store (coalesced,
-          // asynchronous, clipped at the T / N edges by the tensor map) instead of 32-row scattered stores
-          uint8_t* my = sY + ew * C::EPI_TILE_BYTES;
-          if (lane == 0) ptx::bulk_wait_group_read0();  // the previous tile's store has read this buffer
-          __syncwarp();
-#pragma unroll
-          for (int c = 0; c < EPI_COLS; c += 8) {
-            uint32_t w[4];
+          // bf16: with TMA, this warp's 32 x 80 sub-tile goes through shared memory and one tensor store
+          // (coalesced, asynchronous, clipped at the T / N edges by the tensor map); else 16-byte row stores
+          auto pack8 = [&](int c, uint32_t (&w)[4]) {
 #pragma unroll
             for (int h = 0; h < 4; ++h) {
-              const float a0 = (acc[c + 2 * h] * rs) * beta_sm[half * EPI_COLS + c + 2 * h];
-              const float a1 = (acc[c + 2 * h + 1] * rs) * beta_sm[half * EPI_COLS + c + 2 * h + 1];
-              const __nv_bfloat162 bb = __floats2bfloat162_rn(a0, a1);
+              const float2 v = __fmul2_rn(acc2[c / 2 + h], beta2[c / 2 + h]);
+              const __nv_bfloat162 bb = __floats2bfloat162_rn(v.x, v.y);
               w[h] = *reinterpret_cast<const uint32_t*>(&bb);
             }
-            *reinterpret_cast<uint4*>(my + lane * (EPI_COLS * 2) + c * 2) = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-          ptx::fence_proxy_async_shared();
-          __syncwarp();
-          if (lane == 0) {
-            ptx::tma_store_2d(&tmap_y, my, col0, m_blk * BM * kCta + (int)rank * BM + quad * 32);
-            ptx::bulk_commit_group();
+          };
+          if (p.y_tma) {
+            uint8_t* my = sY + ew * C::EPI_TILE_BYTES;
+            if (lane == 0) ptx::bulk_wait_group_read0();  // the previous tile's store has read this buffer
+            __syncwarp();
+            if (trace_epi) gtrace(8 * it + 2, 7);
+#pragma unroll
+            for (int c = 0; c < EPI_COLS; c += 8) {
+              uint32_t w[4];
+              pack8(c, w);
+              *reinterpret_cast<uint4*>(my + lane * (EPI_COLS * 2) + c * 2) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            ptx::fence_proxy_async_shared();
+            if (trace_epi) gtrace(8 * it + 3, 7);
+            __syncwarp();
+            if (lane == 0) {
+              ptx::tma_store_2d(&tmap_y, my, col0, m_blk * BM * kCta + (int)rank * BM + quad * 32);
+              ptx::bulk_commit_group();
+              if (trace_epi) gtrace(8 * it + 4, 7);
+            }
+          } else {
+            __nv_bfloat16* yrow = reinterpret_cast<__nv_bfloat16*>(p.Y) + (int64_t)row * p.ldy;
+#pragma unroll
+            for (int c = 0; c < EPI_COLS; c += 8) {
+              uint32_t w[4];
+              pack8(c, w);
+              const int n = col0 + c;
+              if (n + 7 < p.N) {
+                *reinterpret_cast<uint4*>(yrow + n) = make_uint4(w[0], w[1], w[2], w[3]);
+              } else {
+                const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(w);
+                for (int h = 0; h < 8; ++h)
+                  if (n + h < p.N) yrow[n + h] = e[h];
+              }
+            }
           }
         }
       }
-      if (trace_epi) gtrace(15, 7);
+      if (trace_epi) gtrace(8 * it + 5, 7);
     }
   }
   if constexpr (!kF32Out && !kDebug) {
