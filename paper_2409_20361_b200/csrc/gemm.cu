@@ -62,6 +62,19 @@ __device__ __forceinline__ int gtrace_row(int, int, int) { return -1; }
 __device__ __forceinline__ void gtrace(int, int) {}
 #endif
 
+// Wait flavour of the per-group barriers (experiments: bench/micro/build.sh builds gemm_time with both)
+#ifndef RRS_GEMM_SPIN_EPI
+#define RRS_GEMM_SPIN_EPI 0
+#endif
+// 0: the MMA commits each group's SMEM stage (empty) and the accumulator (tfull) -- two commits per group;
+// 1/2: one commit (tfull) and a promotion thread frees the stage before its TMEM loads / after its release
+#ifndef RRS_GEMM_ONE_COMMIT
+#define RRS_GEMM_ONE_COMMIT 0
+#endif
+#ifndef RRS_GEMM_SPIN_MMA
+#define RRS_GEMM_SPIN_MMA 0
+#endif
+
 namespace gemm {
 constexpr int BM = 128;        // tokens per CTA    (TMEM lanes)
 constexpr int BN = 240;        // outputs per tile  (TMEM columns per accumulator; 256-column slots)
@@ -138,6 +151,9 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
+#if defined(RRS_GEXP) && RRS_GEXP == 4
+    ptx::mbar_init(tempty + 3, 1);  // timeline experiment: a barrier nobody waits on
+#endif
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], kCta * NUM_EPI_WARPS);  // only the leader's copy is used
@@ -201,22 +217,33 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           // use u = acc_iter >> 1 of buffer b needs the (u)-th release (completion #u of tempty[b]); the
           // releases come from both CTAs of a pair (cluster-scope acquire)
           if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
-          else ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
+          else if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
+          else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
         }
         gtrace(trow, 0);
-        ptx::mbar_wait_spin(&full[stage], phase);
+        if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&full[stage], phase);
+        else ptx::mbar_wait(&full[stage], phase);
         gtrace(trow, 1);
         ptx::tc_fence_after();
         // descriptor start addresses advance in 16-byte units: stage offsets, then 32 bytes per K step
         const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
         const uint64_t b_desc = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
+#if defined(RRS_GEXP) && RRS_GEXP == 3
+        // experiment (plain mode, wrong results): alternate the accumulator buffer every group
+        const uint32_t d = tmem_base + (kPlain ? (uint32_t)(kb & 1) : b) * ACC_STRIDE;
+#else
         const uint32_t d = tmem_base + b * ACC_STRIDE;
+#endif
 #pragma unroll
         for (int k = 0; k < BK / 32; ++k) {
           // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier:
           // always accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
           if constexpr (kFp8) {
+#if defined(RRS_GEXP) && RRS_GEXP == 5
+            const uint32_t acc = k > 0;  // experiment (plain mode, wrong results): fresh sum every group
+#else
             const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (k > 0);
+#endif
             if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
             else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
           } else {
@@ -224,12 +251,16 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
           }
         }
+        // (a second tcgen05.commit per group costs ~18 ns of tensor-pipe time, bench/micro GEXP 4)
         if constexpr (kCta == 1) {
-          ptx::mma_commit(&empty[stage]);
+          if (kPlain || !RRS_GEMM_ONE_COMMIT) ptx::mma_commit(&empty[stage]);
           if (!kPlain || kb == p.G - 1) ptx::mma_commit(&tfull[b]);
         } else {
-          ptx::mma_commit_pair(&empty[stage], 0x3);
+          if (kPlain || !RRS_GEMM_ONE_COMMIT) ptx::mma_commit_pair(&empty[stage], 0x3);
           if (!kPlain || kb == p.G - 1) ptx::mma_commit_pair(&tfull[b], 0x3);
+#if defined(RRS_GEXP) && RRS_GEXP == 4
+          else ptx::mma_commit_pair(tempty + 3, 0x3);  // experiment: a second commit every group in plain mode
+#endif
         }
         gtrace(trow, 2);
         if (!kPlain || kb == p.G - 1) ++acc_iter;
@@ -315,9 +346,12 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       for (int g = 0; g < ngroups; ++g) {
         const uint32_t b = acc_iter & 1;
         // RRS: a buffer lands every group, spin for the lowest wake-up latency; plain: once per tile, sleep
-        if constexpr (kPlain) ptx::mbar_wait(&tfull[b], (acc_iter >> 1) & 1);
+        if constexpr (kPlain || !RRS_GEMM_SPIN_EPI) ptx::mbar_wait(&tfull[b], (acc_iter >> 1) & 1);
         else ptx::mbar_wait_spin(&tfull[b], (acc_iter >> 1) & 1);
         ptx::tc_fence_after();
+        // group acc_iter's MMAs are complete, so its SMEM stage (acc_iter % STAGES in the producer's order)
+        // is free: one thread per CTA releases it to this CTA's producer
+        if (RRS_GEMM_ONE_COMMIT == 1 && !kPlain && et == 0) ptx::mbar_arrive(&empty[acc_iter % STAGES]);
         const bool trace_me = lane == 0 && (ew == 0 || ew == NUM_EPI_WARPS - 1);
         const int trow = gtrace_row(it, g, p.G);
         if (trace_me) gtrace(trow, ew == 0 ? 3 : 5);
@@ -403,6 +437,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(b ? tempty_addr1 : tempty_addr0);
         }
+        if (RRS_GEMM_ONE_COMMIT == 2 && !kPlain && et == 0) ptx::mbar_arrive(&empty[acc_iter % STAGES]);
         ++acc_iter;
       }
       // ---- epilogue: Y = acc * beta_n  (acc already carries alpha_t * out_scale)

@@ -44,7 +44,11 @@ struct ColmaxSmem {
   static_assert(2 * P::TILE * 4 <= TILE_D && K * 4 <= 2 * STAGE, "fused quantisation staging");
 };
 
-constexpr int kColmaxCluster = 8;  // CTAs that combine their column maxima through DSMEM before the atomics
+// CTAs that combine their column maxima through DSMEM before the atomics.  2^m plans run several CTAs per SM,
+// so clusters of 8 pack densely; the 28*2^m plan runs one 256-thread CTA per SM, where a cluster of 8 must fit
+// inside one GPC and only 15 such clusters (120 of 148 SMs) are co-resident -- pairs use every SM.
+template <int K>
+__host__ __device__ constexpr int colmax_cluster() { return FwhtPlan<K>::kPow2 ? 8 : 2; }
 
 // The FWHT pass (rows a1-a2): every CTA of the (persistent, clustered) grid transforms its rows, writes X~
 // f32 and, unless chan_max_bits is null, folds its column maxima into chan_max (DSMEM cluster reduction +
@@ -123,7 +127,7 @@ RRS_DEVICE void fwht_phase(const uint16_t* __restrict__ X, int64_t T, unsigned* 
   ptx::cluster_sync();
   trace(0, 13);
   const uint32_t rank = ptx::cluster_ctarank();
-  constexpr int SLICE = K / kColmaxCluster;
+  constexpr int SLICE = K / colmax_cluster<K>();
   constexpr int PER_THREAD = (SLICE + P::THREADS - 1) / P::THREADS;
   uint32_t mx[PER_THREAD];
 #pragma unroll
@@ -132,7 +136,7 @@ RRS_DEVICE void fwht_phase(const uint16_t* __restrict__ X, int64_t T, unsigned* 
     uint32_t m = 0u;
     if (threadIdx.x + i * P::THREADS < SLICE) {
 #pragma unroll
-      for (uint32_t r = 0; r < kColmaxCluster; ++r) m = max(m, ptx::ld_dsmem_u32(cmx + c, r));
+      for (uint32_t r = 0; r < colmax_cluster<K>(); ++r) m = max(m, ptx::ld_dsmem_u32(cmx + c, r));
     }
     mx[i] = m;
   }
@@ -149,7 +153,7 @@ RRS_DEVICE void fwht_phase(const uint16_t* __restrict__ X, int64_t T, unsigned* 
 }
 
 template <int K>
-__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
+__global__ void __cluster_dims__(colmax_cluster<K>(), 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
 fwht_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
                    float* __restrict__ Xr) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -283,7 +287,7 @@ RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, boo
 // barrier (the grid is sized to be co-resident: max active clusters), then the quantisation pass on the same
 // CTAs and the same rows (their X~ is still in L2).  `counter` (next to chan_max, zeroed with it) counts CTAs.
 template <int K>
-__global__ void __cluster_dims__(kColmaxCluster, 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
+__global__ void __cluster_dims__(colmax_cluster<K>(), 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
 prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
                       float* __restrict__ Xr, unsigned* __restrict__ counter, const int32_t* __restrict__ perm,
                       float* __restrict__ s_group_out, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
@@ -308,7 +312,7 @@ prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __res
   ptx::cluster_sync();
   if (ptx::cluster_ctarank() == 0 && threadIdx.x == 0) {
     atomicAdd(counter, 1u);
-    const unsigned nclusters = gridDim.x / kColmaxCluster;
+    const unsigned nclusters = gridDim.x / colmax_cluster<K>();
     unsigned v;
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
@@ -335,9 +339,9 @@ prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __res
     // chan_max -> every CTA of the cluster: each rank fetches one eighth once from L2 and multicasts it
     ptx::mbar_arrive_expect_tx(&bar[2], K * 4);
     const uint32_t rank = ptx::cluster_ctarank();
-    constexpr int SL = K / kColmaxCluster;
+    constexpr int SL = K / colmax_cluster<K>();
     ptx::bulk_load_multicast(cms + rank * SL, chan_max_bits + rank * SL, SL * 4, &bar[2],
-                             (uint16_t)((1u << kColmaxCluster) - 1));
+                             (uint16_t)((1u << colmax_cluster<K>()) - 1));
     if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
     if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
   }
@@ -476,17 +480,17 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
   static int max_clusters[2] = {0, 0};  // per K instantiation, cached
   if (max_clusters[0] == 0) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kColmaxCluster * 1024);
+    cfg.gridDim = dim3(colmax_cluster<K>() * 1024);
     cfg.blockDim = dim3(P::THREADS);
     cfg.dynamicSmemBytes = smem;
     int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = nsm / kColmaxCluster;
+    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = nsm / colmax_cluster<K>();
     max_clusters[0] = n;
   }
   const int64_t tiles = (T + P::R - 1) / P::R;
   if (tiles == 0) return cudaSuccess;
-  const int64_t clusters = std::min<int64_t>(max_clusters[0], (tiles + kColmaxCluster - 1) / kColmaxCluster);
-  const int grid = (int)clusters * kColmaxCluster;  // whole clusters (CTAs without a tile are fine)
+  const int64_t clusters = std::min<int64_t>(max_clusters[0], (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>());
+  const int grid = (int)clusters * colmax_cluster<K>();  // whole clusters (CTAs without a tile are fine)
   kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr);
   return cudaGetLastError();
 }
@@ -504,7 +508,7 @@ static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, fl
   static int max_clusters = 0;
   if (max_clusters == 0) {
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(kColmaxCluster * 1024);
+    cfg.gridDim = dim3(colmax_cluster<K>() * 1024);
     cfg.blockDim = dim3(P::THREADS);
     cfg.dynamicSmemBytes = smem;
     int n = 0;
@@ -512,8 +516,8 @@ static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, fl
     max_clusters = n;
   }
   const int64_t tiles = (T + P::R - 1) / P::R;
-  const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + kColmaxCluster - 1) / kColmaxCluster));
-  const int grid = (int)clusters * kColmaxCluster;
+  const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>()));
+  const int grid = (int)clusters * colmax_cluster<K>();
   kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr, counter, perm, s_group, Xq, Xq8, scale, (int)e4m3);
   return cudaGetLastError();
 }
