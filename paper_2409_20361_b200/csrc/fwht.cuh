@@ -36,20 +36,21 @@ struct FwhtPlan {
   static constexpr int A = kPow2 ? 1 : 28;          // H28 factor
   static constexpr int NP2 = K / A;                  // power-of-two part
   static constexpr int LOGN = ilog2_c(NP2);
-  static constexpr int B = kPow2 ? 5 : 6;            // bits per pass
+  static constexpr int B = 5;                        // bits per pass (E = 32 doubles per thread)
   static constexpr int E = 1 << B;                   // values per thread in the 2^m passes
   static constexpr int TP2 = K / E;                  // threads per row in the 2^m passes
-  static constexpr int TH28 = kPow2 ? 0 : NP2 / 2;   // threads per row in the H28 pass (2 groups of 28)
+  static constexpr int TH28 = kPow2 ? 0 : NP2;       // threads per row in the H28 pass (one 28-vector each)
   static constexpr int TPR = max_c(TP2, TH28);       // threads per row
   static constexpr int R = kPow2 ? max_c(1, 128 / TP2) : 1;  // rows per CTA tile (>= 4 warps per CTA)
   static constexpr int THREADS = ((R * TPR + 31) / 32) * 32;
-  static constexpr int MIN_BLOCKS = kPow2 ? max_c(1, 512 / THREADS) : 1;  // 16 warps/SM -> <= 128 regs
+  static constexpr int MIN_BLOCKS = max_c(1, 512 / THREADS);  // 16 warps/SM -> <= 128 regs
   static constexpr int HI = LOGN - (B - 3);          // pass 0: bits [0,3) and [HI, LOGN)
-  static constexpr int SLOTS = kPow2 ? E : 56;       // values per thread after the last pass
+  static constexpr int SLOTS = kPow2 ? E : 28;       // values per thread after the last pass
   static constexpr int TILE = R * K;                 // elements per CTA tile
-  // padding coefficients (tools/smem_pad_search.py): 2^m: i + i/16 + 4(i>>7); 28*2^m: + 4(i>>6) + 4(i>>9)
-  static constexpr int PAD_S1 = kPow2 ? 7 : 6, PAD_C1 = 4;
-  static constexpr int PAD_S2 = 9, PAD_C2 = kPow2 ? 0 : 4;
+  // padding coefficients (tools/smem_pad_search.py): 2^m: i + i/16 + 4(i>>7); 28*512: i + i/16;
+  // 28*256: i + i/16 + 4(i>>6) + 4(i>>8)
+  static constexpr int PAD_S1 = kPow2 ? 7 : 6, PAD_C1 = (kPow2 || NP2 <= 256) ? 4 : 0;
+  static constexpr int PAD_S2 = kPow2 ? 9 : 8, PAD_C2 = (!kPow2 && NP2 <= 256) ? 4 : 0;
   static constexpr int TILE_PAD = TILE + TILE / 16 + PAD_C1 * (TILE >> PAD_S1) + PAD_C2 * (TILE >> PAD_S2) + 8;
   static_assert(A * NP2 == K, "K must be 2^m or 28*2^m");
   static_assert(LOGN >= 7, "power-of-two part must be >= 128");
@@ -105,28 +106,45 @@ RRS_DEVICE constexpr int chi13(int a) {
   return a == 0 ? 0 : ((a == 1 || a == 3 || a == 4 || a == 9 || a == 10 || a == 12) ? 1 : -1);
 }
 
-template <int OFF, int E>
-RRS_DEVICE void h28_apply(double (&v)[E]) {
-  double u0[14], u1[14], w0[14], w1[14];
+// y = H28 . v for the 28 values v[0..27] (pairs (x0_i, x1_i) = (v[2i], v[2i+1]), i < 14), rounded once to f32.
+// With s_i = x0_i + x1_i, d_i = x0_i - x1_i the Paley-II form above gives
+//   y[2j]   = s_j + (S d)_j,   y[2j+1] = d_j - (S s)_j,
+//   (S u)_0 = U := sum_{i=1..13} u_i,   (S u)_j = u_0 + 2 R_j(u) - U + u_j  (j >= 1),
+// where R_j(u) = sum over the 6 quadratic residues r of u_{1+((j-1+r) mod 13)}: chi13 is +1 on the residues
+// and -1 on the non-residues, so sum_{i != j} chi13(i-j) u_i = 2 R_j(u) - (U - u_j).  ~10 DADD per output
+// instead of ~15.  Every intermediate is a signed integer combination of the inputs no larger in magnitude
+// than the final sums' bound (|2 R_j| <= 12 max|u|, |U| <= 13 max|u|), so it stays exact under R3.
+RRS_DEVICE constexpr int qr13(int k) {  // the quadratic residues mod 13
+  return k == 0 ? 1 : k == 1 ? 3 : k == 2 ? 4 : k == 3 ? 9 : k == 4 ? 10 : 12;
+}
+template <int E, class Emit>
+RRS_DEVICE void h28_lean(double (&v)[E], Emit&& emit) {
 #pragma unroll
   for (int i = 0; i < 14; ++i) {
-    const double x0 = v[OFF + 2 * i], x1 = v[OFF + 2 * i + 1];
-    u0[i] = x0 - x1;   // A2 row 0: ( 1, -1)
-    u1[i] = -x0 - x1;  // A2 row 1: (-1, -1)
-    w0[i] = x0 + x1;   // B2 row 0: ( 1,  1)
-    w1[i] = x0 - x1;   // B2 row 1: ( 1, -1)
+    const double a = v[2 * i], b = v[2 * i + 1];
+    v[2 * i] = a + b;      // s_i
+    v[2 * i + 1] = a - b;  // d_i
   }
+  double S = 0.0, D = 0.0;
 #pragma unroll
-  for (int j = 0; j < 14; ++j) {
-    double s0 = w0[j], s1 = w1[j];
+  for (int i = 1; i < 14; ++i) {
+    S += v[2 * i];
+    D += v[2 * i + 1];
+  }
+  emit(0, __double2float_rn(v[0] + D));
+  emit(1, __double2float_rn(v[1] - S));
 #pragma unroll
-    for (int i = 0; i < 14; ++i) {
-      if (i == j) continue;
-      const int sg = (j == 0 || i == 0) ? 1 : chi13((i - 1) - (j - 1));
-      if (sg > 0) { s0 += u0[i]; s1 += u1[i]; } else { s0 -= u0[i]; s1 -= u1[i]; }
+  for (int j = 1; j < 14; ++j) {
+    double rs = 0.0, rd = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) {
+      const int i = 1 + ((j - 1 + qr13(k)) % 13);
+      rs += v[2 * i];
+      rd += v[2 * i + 1];
     }
-    v[OFF + 2 * j] = s0;
-    v[OFF + 2 * j + 1] = s1;
+    const double sj = v[2 * j], dj = v[2 * j + 1];
+    emit(2 * j, __double2float_rn(fma(2.0, rd, (sj + dj) + (v[1] - D))));
+    emit(2 * j + 1, __double2float_rn(dj - fma(2.0, rs, (sj + v[0]) - S)));
   }
 }
 
@@ -139,8 +157,8 @@ RRS_DEVICE int reg_index(int tp, int j) {
   if constexpr (L == -1) {
     return p0_index<P>(tp, j);
   } else if constexpr (L == -2) {
-    // group u (2 per thread) = column offset bb inside the 2^m chunk; register a = chunk index
-    return (j % 28) * P::NP2 + tp + P::TH28 * (j / 28);
+    // register j = chunk index; the thread's column offset inside the 2^m chunk is tp
+    return j * P::NP2 + tp;
   } else {
     constexpr int r = min_c(P::B, P::HI - L);
     return p2_index<P, L, r>(tp, j >> r, j & ((1 << r) - 1));
@@ -149,22 +167,22 @@ RRS_DEVICE int reg_index(int tp, int j) {
 
 template <class P, int L>
 RRS_DEVICE void store_layout(double* sm, int rr, int tp, const double (&v)[P::E]) {
-  constexpr int n = (L == -2) ? 56 : P::E;
+  constexpr int n = (L == -2) ? 28 : P::E;
 #pragma unroll
   for (int j = 0; j < n; ++j) sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))] = v[j];
 }
 
 template <class P, int L>
 RRS_DEVICE void load_layout(const double* sm, int rr, int tp, double (&v)[P::E]) {
-  constexpr int n = (L == -2) ? 56 : P::E;
+  constexpr int n = (L == -2) ? 28 : P::E;
 #pragma unroll
   for (int j = 0; j < n; ++j) v[j] = sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))];
 }
 
 // The middle passes [b, HI) following a pass with layout PL; finally the H28 pass.  Ends with v in the
 // layout last_layout<P>().  Every thread of the CTA must call it.
-template <class P, int PL, int b>
-RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, double (&v)[P::E]) {
+template <class P, int PL, int b, class Emit>
+RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, double (&v)[P::E], Emit&& emit) {
   if constexpr (b < P::HI) {
     constexpr int r = min_c(P::B, P::HI - b);
     if (p2act) store_layout<P, PL>(sm, rr, tp, v);
@@ -174,14 +192,13 @@ RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, d
       butterflies<r>(v);
     }
     __syncthreads();  // the tile is rewritten by the next pass (or by the next row)
-    fwht_rest<P, b, b + r>(sm, rr, tp, p2act, h28act, v);
+    fwht_rest<P, b, b + r>(sm, rr, tp, p2act, h28act, v, emit);
   } else if constexpr (!P::kPow2) {
     if (p2act) store_layout<P, PL>(sm, rr, tp, v);
     __syncthreads();
     if (h28act) {
       load_layout<P, -2>(sm, 0, threadIdx.x, v);  // H28 layout is indexed by the CTA thread
-      h28_apply<0>(v);
-      h28_apply<28>(v);
+      h28_lean(v, emit);
     }
     __syncthreads();
   }
@@ -198,17 +215,19 @@ __host__ __device__ constexpr int last_layout() {
   return last;
 }
 
-// Transform the R-row bf16 tile `stage` (shared memory, raw bits, row-major [R][K]) into v[].
-// Afterwards thread t holds, for j < SLOTS, the exact rotated value of row-local column
-// out_col<P>(tp, j) of tile row rr (t = rr * TP2 + tp in the 2^m passes; t = tp for H28).
+// Transform the R-row bf16 tile `stage` (shared memory, raw bits, row-major [R][K]); v[] is scratch.
+// For every j < SLOTS of an active thread (out_active), calls emit(j, y) with y the correctly rounded (f32)
+// rotated value of row-local column out_col<P>(tp, j) of tile row rr (t = rr * TP2 + tp in the 2^m passes;
+// t = tp for H28).  rr and tp are set before the first emit.
 // active_rows masks rows beyond the matrix (their lanes still run, on whatever the stage holds).
-template <class P>
-RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], int& rr, int& tp) {
+template <class P, class Emit>
+RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], int& rr, int& tp, Emit&& emit) {
   const int t = threadIdx.x;
   const bool p2act = t < P::R * P::TP2;
   const bool h28act = !P::kPow2 && t < P::TH28;
   rr = P::kPow2 ? (p2act ? t / P::TP2 : 0) : 0;
   const int tp2 = p2act ? t % P::TP2 : 0;
+  tp = P::kPow2 ? tp2 : t;
   if (p2act) {
     // bf16 -> f32 (placing the 16 bits high) -> f64 (F2F, exact for every finite value incl. subnormals)
     const uint16_t* row = stage + rr * P::K;
@@ -224,8 +243,13 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], 
     }
     butterflies<P::B>(v);
   }
-  fwht_rest<P, -1, 3>(sm, rr, tp2, p2act, h28act, v);
-  tp = P::kPow2 ? tp2 : t;
+  fwht_rest<P, -1, 3>(sm, rr, tp2, p2act, h28act, v, emit);
+  if constexpr (P::kPow2) {
+    if (p2act) {
+#pragma unroll
+      for (int j = 0; j < P::SLOTS; ++j) emit(j, __double2float_rn(v[j]));
+    }
+  }
 }
 
 template <class P>

@@ -89,20 +89,24 @@ RRS_DEVICE void fwht_phase(const uint16_t* __restrict__ X, int64_t T, unsigned* 
     ptx::mbar_wait(&bar[buf], (it >> 1) & 1);
     trace(0, 1 + 2 * (it < 5 ? it : 5));
     double v[P::E];
-    int rr, tp;
-    fwht_tile<P>(stage + buf * P::TILE, sm, v, rr, tp);  // ends with __syncthreads: stage[buf] is free
-    trace(0, 2 + 2 * (it < 5 ? it : 5));
-    if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
-    const int64_t row = tile * P::R + rr;
-    if (act && row < T) {
-      float* xr = Xr + row * K;
-#pragma unroll
-      for (int j = 0; j < P::SLOTS; ++j) {
-        const float f = __double2float_rn(v[j]);
+    int rr = 0, tp = 0;
+    float* xr = nullptr;
+    bool live = false;
+    // X~ stores and column maxima as the values are produced (rr / tp are set before the first call)
+    auto emit = [&](int j, float f) {
+      if (!xr) {
+        const int64_t row = tile * P::R + rr;
+        live = row < T;
+        xr = Xr + row * K;
+      }
+      if (live) {
         cm[j] = fmaxf(cm[j], fabsf(f));
         xr[out_col<P>(tp, j)] = f;
       }
-    }
+    };
+    fwht_tile<P>(stage + buf * P::TILE, sm, v, rr, tp, emit);  // ends with __syncthreads: stage[buf] is free
+    trace(0, 2 + 2 * (it < 5 ? it : 5));
+    if (threadIdx.x == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
   }
   trace(0, 12);
   ptx::pdl_launch_dependents();

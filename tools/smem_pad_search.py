@@ -14,10 +14,10 @@ def plan(K):
     A = 1 if pow2 else 28
     NP2 = K // A
     LOGN = NP2.bit_length() - 1
-    B = 5 if pow2 else 6
+    B = 5
     E = 1 << B
     TP2 = K // E
-    TH28 = 0 if pow2 else NP2 // 2
+    TH28 = 0 if pow2 else NP2  # one 28-vector per thread in the H28 pass
     HI = LOGN - (B - 3)
     return dict(K=K, pow2=pow2, NP2=NP2, LOGN=LOGN, B=B, E=E, TP2=TP2, TH28=TH28, HI=HI)
 
@@ -42,7 +42,7 @@ def layouts(P):
                     P["E"], P["TP2"]))
         b += r
     if not P["pow2"]:
-        out.append(("h28", lambda tp, j: (j % 28) * P["NP2"] + tp + P["TH28"] * (j // 28), 56, P["TH28"]))
+        out.append(("h28", lambda tp, j: j * P["NP2"] + tp, 28, P["TH28"]))
     return out
 
 
