@@ -6,7 +6,8 @@
  * readings R1..R24 of DESIGN.md §3 where the paper is silent.
  *
  * Notation: T tokens (paper's N), K input features, N output features (paper's M),
- * group size L = 128 (= GEMM K-block), G = K / L groups.
+ * group size L = 128 (= GEMM K-block; any power of two in [32, 1024] is accepted, the
+ * group sizes of the paper's Table 4 ablation), G = K / L groups.
  *
  * Conventions shared by every entry point
  *   - Array arguments are DEVICE pointers (CUDA global memory) allocated and owned by the caller;
@@ -27,7 +28,7 @@
  *     returns without synchronising the host.  Asynchronous device faults surface on a later CUDA call.
  *   - Validation happens before any launch; on error nothing is enqueued, the status is returned
  *     and rrs_last_error() (thread-local) describes it.
- *   - Supported shapes: group == 128; K % 128 == 0 and K in {128,256,...,16384} (2^m) or
+ *   - Supported shapes: group a power of two in [32, 1024] dividing K; K % 128 == 0 and K in {128,256,...,16384} (2^m) or
  *     {7168, 14336} (28*2^m, R2); T >= 0; N >= 1.  All pointers 16-byte aligned.
  *   - X must be bf16 and satisfy the exactness precondition of DESIGN.md R3 (per row, exponent span
  *     of the nonzero |x| <= 45 - ceil(log2 K)); NaN/Inf inputs are undefined behaviour (not checked).
@@ -46,8 +47,9 @@ extern "C" {
 
 typedef enum {
   RRS_OK = 0,
-  RRS_ERR_INVALID_ARGUMENT = 1,  /* null pointer where required, negative size, group != 128 */
-  RRS_ERR_UNSUPPORTED_SHAPE = 2, /* K not 2^m / 28*2^m, K % group != 0 (R7) */
+  RRS_ERR_INVALID_ARGUMENT = 1,  /* null pointer where required, negative size, group not a power of two
+                                    in [32, 1024] */
+  RRS_ERR_UNSUPPORTED_SHAPE = 2, /* K not 2^m / 28*2^m, K % group != 0 or K % 128 != 0 (R7) */
   RRS_ERR_MISALIGNED = 3,        /* pointer or leading dimension not 16-byte aligned */
   RRS_ERR_WORKSPACE_TOO_SMALL = 4,
   RRS_ERR_ARCH = 5,              /* current device is not sm_100 (B200) */

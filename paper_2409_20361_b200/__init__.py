@@ -41,8 +41,9 @@ class RRSLinear:
     """Y = RRS-A4W4(X) @ W^T for a bf16 nn.Linear weight W[N][K] (column shard when comm is given)."""
 
     def __init__(self, W: torch.Tensor, perm: torch.Tensor, comm=None, world: int = 1, rank: int = 0,
-                 keep_packed: bool = False, i8: bool = False, stream=None):
+                 keep_packed: bool = False, i8: bool = False, group: int = GROUP, stream=None):
         N, K = W.shape
+        self.group = group  # smoothing group (P:189: 128; SURVEY §8 f3: any power of two in [32, 1024])
         self.K, self.N_total = K, N
         self.comm, self.world, self.rank = comm, world, rank
         lo, hi = shard_rows(N, world, rank)
@@ -57,7 +58,7 @@ class RRSLinear:
         self._ws = None
 
     def workspace(self, T: int, device) -> torch.Tensor:
-        need = rrs_workspace_bytes(T, self.N_total, self.K, GROUP, self.world)
+        need = rrs_workspace_bytes(T, self.N_total, self.K, self.group, self.world)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=device)
         return self._ws
@@ -67,7 +68,7 @@ class RRSLinear:
         if Y is None:
             Y = torch.empty((T, self.N_total), dtype=out_dtype, device=X.device)
         rrs_linear(X, self.perm, self.Wop, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
-                   comm=self.comm, i8=self.i8, stream=stream)
+                   comm=self.comm, group=self.group, i8=self.i8, stream=stream)
         return Y
 
 

@@ -71,10 +71,19 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// Smoothing group: the paper's 128 = the GEMM K-block, and the Table-4 sizes; a power of
+// two in [32, 1024] (a multiple of the 32-deep MMA K-step that divides or is divided by the 128-deep K-block)
+rrs_status check_group(int64_t K, int32_t group) {
+  if (group < 32 || group > 1024 || (group & (group - 1)))
+    return fail(RRS_ERR_INVALID_ARGUMENT, "group=%d: need a power of two in [32, 1024] (128 = P:189)", group);
+  if (K <= 0 || K % group || K % 128)
+    return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld must be a positive multiple of group %d and of 128", (long long)K, group);
+  return RRS_OK;
+}
+
 rrs_status check_shape(int64_t T, int64_t K, int32_t group) {
   if (T < 0) return fail(RRS_ERR_INVALID_ARGUMENT, "T=%lld < 0", (long long)T);
-  if (group != 128) return fail(RRS_ERR_INVALID_ARGUMENT, "group=%d: only 128 is supported (P:189)", group);
-  if (K <= 0 || K % group) return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld not a positive multiple of group %d", (long long)K, group);
+  if (rrs_status s = check_group(K, group)) return s;
   if (!rrs::prologue_supports_k(K))
     return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld: need 2^m in [128,16384] or 28*2^m in {7168,14336}", (long long)K);
   return RRS_OK;
@@ -221,7 +230,7 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
     e = rrs::launch_fwht_colmax(Wb + n0 * K, rows, K, nullptr, tmp, nsm, st);
     if (e == cudaSuccess)
       e = rrs::launch_smooth_quant(tmp, rows, K, perm, nullptr, nullptr, Wq ? Wq + n0 * (K / 2) : nullptr,
-                                   Wq8 ? Wq8 + n0 * K : nullptr, w_scale + n0, e4m3, nsm, st);
+                                   Wq8 ? Wq8 + n0 * K : nullptr, w_scale + n0, e4m3, 128, nsm, st);
   }
   cudaError_t e2 = cudaFreeAsync(tmp, st);
   if (e != cudaSuccess) return cuda_fail(e, "weight preparation kernels");
@@ -230,7 +239,7 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
 
 static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* perm, uint8_t* Xq, int8_t* Xq8,
                            float* x_scale, float* s_group, float* chan_max, unsigned* counter, float* Xr, bool e4m3,
-                           int nsm, cudaStream_t st) {
+                           int group, int nsm, cudaStream_t st) {
   // chan_max (and the fused kernel's CTA counter) start at zero; one memset when they are contiguous
   const bool contiguous = reinterpret_cast<unsigned*>(chan_max) + K == counter;
   cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * (contiguous ? K + 1 : K), st);
@@ -238,14 +247,14 @@ static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* p
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
   if (T > 0 && rrs::prologue_fused_supports_k(K)) {
     e = rrs::launch_prologue_fused(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
-                                   counter, perm, s_group, Xq, Xq8, x_scale, e4m3, nsm, st);
+                                   counter, perm, s_group, Xq, Xq8, x_scale, e4m3, group, nsm, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_fused_kernel");
   }
   e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
                               nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "fwht_colmax_kernel");
   e = rrs::launch_smooth_quant(Xr, T, K, perm, reinterpret_cast<const unsigned*>(chan_max), s_group, Xq, Xq8,
-                               x_scale, e4m3, nsm, st);
+                               x_scale, e4m3, group, nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "smooth_quant_kernel");
   return RRS_OK;
 }
@@ -269,14 +278,13 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
   if (!aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   if (!chan_max) chan_max = w.chan_max;
   return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, reinterpret_cast<unsigned*>(w.chan_max) + K,
-                  w.Xr, (flags & RRS_OPERAND_I8) == 0, nsm, static_cast<cudaStream_t>(stream));
+                  w.Xr, (flags & RRS_OPERAND_I8) == 0, group, nsm, static_cast<cudaStream_t>(stream));
 }
 
 static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int8_t* Wq8, const float* w_scale,
                               int64_t T, int64_t N, int64_t K, int32_t group, const void* Y, int64_t ldy) {
   if (T < 0 || N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "T=%lld N=%lld", (long long)T, (long long)N);
-  if (group != 128) return fail(RRS_ERR_INVALID_ARGUMENT, "group=%d: only 128 supported", group);
-  if (K <= 0 || K % group) return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld", (long long)K);
+  if (rrs_status s = check_group(K, group)) return s;
   if (T > 0 && (!Xq8 || !x_scale || !Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!Wq8 || !w_scale) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (ldy < N) return fail(RRS_ERR_INVALID_ARGUMENT, "ldy=%lld < N=%lld", (long long)ldy, (long long)N);
@@ -326,7 +334,7 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max,
-                              reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, e4m3, nsm, st))
+                              reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, e4m3, group, nsm, st))
     return s;
   if (T == 0) return RRS_OK;
   const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
@@ -427,7 +435,8 @@ rrs_status rrs_debug_group_partials(const uint8_t* Xop, const uint8_t* Wop, int6
   if (!P) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   // the GEMM needs valid scale pointers; partials do not depend on them: use a scratch Y in P's tail? No:
   // the debug launch passes P and a null Y; the kernel skips the Y store when Y == nullptr.
-  if (T < 0 || N < 1 || group != 128 || K <= 0 || K % group) return fail(RRS_ERR_INVALID_ARGUMENT, "shape");
+  if (T < 0 || N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "shape");
+  if (rrs_status s = check_group(K, group)) return s;
   if (!aligned16(Xq8) || !aligned16(Wq8)) return fail(RRS_ERR_MISALIGNED, "alignment");
   if (T == 0) return RRS_OK;
   rrs::GemmArgs a{Xq8, nullptr, nullptr, Wq8, nullptr, T, N, K, group, 1.0f, false, (flags & RRS_OPERAND_I8) == 0,

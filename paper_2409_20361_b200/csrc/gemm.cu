@@ -66,11 +66,6 @@ __device__ __forceinline__ void gtrace(int, int) {}
 #ifndef RRS_GEMM_SPIN_EPI
 #define RRS_GEMM_SPIN_EPI 0
 #endif
-// 0: the MMA commits each group's SMEM stage (empty) and the accumulator (tfull) -- two commits per group;
-// 1/2: one commit (tfull) and a promotion thread frees the stage before its TMEM loads / after its release
-#ifndef RRS_GEMM_ONE_COMMIT
-#define RRS_GEMM_ONE_COMMIT 0
-#endif
 #ifndef RRS_GEMM_SPIN_MMA
 #define RRS_GEMM_SPIN_MMA 0
 #endif
@@ -83,7 +78,7 @@ constexpr int NUM_EPI_WARPS = 12;
 constexpr int EPI_COLS = BN / (NUM_EPI_WARPS / 4);  // columns per promotion thread (80)
 constexpr int ACC_STRIDE = 256;  // TMEM column offset between the two accumulator buffers
 constexpr int THREADS = 64 + NUM_EPI_WARPS * 32;
-constexpr int MAX_G = 128;                 // K <= 16384
+constexpr int MAX_G = 512;                 // smoothing groups per row: K / group <= 512
 
 template <int kCta>
 struct Cfg {
@@ -105,7 +100,8 @@ struct GemmParams {
   const float* x_scale;
   const float* s_group;
   const float* w_scale;
-  int T, N, K, G;
+  int T, N, K, G;   // G = K / group smoothing groups
+  int KB, gk;       // K-blocks of 128, MMA K-steps (of 32) per group
   int num_m, num_n, num_tiles;
   float out_scale;
   void* Y;
@@ -151,9 +147,6 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-#if defined(RRS_GEXP) && RRS_GEXP == 4
-    ptx::mbar_init(tempty + 3, 1);  // timeline experiment: a barrier nobody waits on
-#endif
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], kCta * NUM_EPI_WARPS);  // only the leader's copy is used
@@ -183,7 +176,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       for (int tile = blockIdx.x / kCta; tile < p.num_tiles; tile += gridDim.x / kCta) {
         const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
         const int row0 = m_blk * BM * kCta + (int)rank * BM, wrow0 = n_blk * BN + (int)rank * C::B_ROWS;
-        for (int kb = 0; kb < p.G; ++kb) {
+        for (int kb = 0; kb < p.KB; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (kCta == 1) {
             ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
@@ -209,17 +202,13 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     uint32_t acc_iter = 0;  // number of accumulator buffers filled so far
     int it = 0;             // local tile counter (timeline only)
     const uint64_t a_desc0 = ptx::smem_desc_sw128(sA), b_desc0 = ptx::smem_desc_sw128(sB);
+    // smoothing groups of gk = group / 32 MMA K-steps (4 for the paper's 128 = one K-block; the other
+    // Table-4 sizes close a group inside a K-block (32, 64) or after several (256+))
+    const int gk = p.gk;
+    int ks = 0;  // K-steps of the current group issued so far
     for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
-      for (int kb = 0; kb < p.G; ++kb, it += (kb == p.G)) {
-        const int trow = gtrace_row(it, kb, p.G);
-        const uint32_t b = acc_iter & 1;
-        if (kPlain ? kb == 0 : true) {
-          // use u = acc_iter >> 1 of buffer b needs the (u)-th release (completion #u of tempty[b]); the
-          // releases come from both CTAs of a pair (cluster-scope acquire)
-          if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
-          else if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
-          else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
-        }
+      for (int kb = 0; kb < p.KB; ++kb, it += (kb == p.KB)) {
+        const int trow = gtrace_row(it, kb, p.KB);
         gtrace(trow, 0);
         if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&full[stage], phase);
         else ptx::mbar_wait(&full[stage], phase);
@@ -228,42 +217,45 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         // descriptor start addresses advance in 16-byte units: stage offsets, then 32 bytes per K step
         const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
         const uint64_t b_desc = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
-#if defined(RRS_GEXP) && RRS_GEXP == 3
-        // experiment (plain mode, wrong results): alternate the accumulator buffer every group
-        const uint32_t d = tmem_base + (kPlain ? (uint32_t)(kb & 1) : b) * ACC_STRIDE;
-#else
-        const uint32_t d = tmem_base + b * ACC_STRIDE;
-#endif
 #pragma unroll
         for (int k = 0; k < BK / 32; ++k) {
+          const uint32_t b = acc_iter & 1;
+          if (kPlain ? (kb == 0 && k == 0) : ks == 0) {
+            // a new accumulation into buffer b: use u = acc_iter >> 1 of it needs the u-th release (completion
+            // #u of tempty[b]); the releases come from both CTAs of a pair (cluster-scope acquire for int8)
+            if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
+            else if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
+            else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
+            ptx::tc_fence_after();
+          }
+          const uint32_t d = tmem_base + b * ACC_STRIDE;
           // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier:
           // always accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
           if constexpr (kFp8) {
-#if defined(RRS_GEXP) && RRS_GEXP == 5
-            const uint32_t acc = k > 0;  // experiment (plain mode, wrong results): fresh sum every group
-#else
-            const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (k > 0);
-#endif
+            const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (ks > 0);
             if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
             else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
           } else {
             if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
             else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
           }
+          if (!kPlain && ++ks == gk) {  // group complete: hand the buffer to the promotion warps
+            if constexpr (kCta == 1) ptx::mma_commit(&tfull[b]);
+            else ptx::mma_commit_pair(&tfull[b], 0x3);
+            ++acc_iter;
+            ks = 0;
+          }
         }
-        // (a second tcgen05.commit per group costs ~18 ns of tensor-pipe time, bench/micro GEXP 4)
-        if constexpr (kCta == 1) {
-          if (kPlain || !RRS_GEMM_ONE_COMMIT) ptx::mma_commit(&empty[stage]);
-          if (!kPlain || kb == p.G - 1) ptx::mma_commit(&tfull[b]);
-        } else {
-          if (kPlain || !RRS_GEMM_ONE_COMMIT) ptx::mma_commit_pair(&empty[stage], 0x3);
-          if (!kPlain || kb == p.G - 1) ptx::mma_commit_pair(&tfull[b], 0x3);
-#if defined(RRS_GEXP) && RRS_GEXP == 4
-          else ptx::mma_commit_pair(tempty + 3, 0x3);  // experiment: a second commit every group in plain mode
-#endif
+        // the SMEM stage is free once these MMAs complete (a second commit per group costs ~18 ns of
+        // tensor-pipe time, but freeing the stage from a promotion thread instead was slower)
+        if constexpr (kCta == 1) ptx::mma_commit(&empty[stage]);
+        else ptx::mma_commit_pair(&empty[stage], 0x3);
+        if (kPlain && kb == p.KB - 1) {
+          if constexpr (kCta == 1) ptx::mma_commit(&tfull[acc_iter & 1]);
+          else ptx::mma_commit_pair(&tfull[acc_iter & 1], 0x3);
+          ++acc_iter;
         }
         gtrace(trow, 2);
-        if (!kPlain || kb == p.G - 1) ++acc_iter;
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
@@ -351,7 +343,6 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         ptx::tc_fence_after();
         // group acc_iter's MMAs are complete, so its SMEM stage (acc_iter % STAGES in the producer's order)
         // is free: one thread per CTA releases it to this CTA's producer
-        if (RRS_GEMM_ONE_COMMIT == 1 && !kPlain && et == 0) ptx::mbar_arrive(&empty[acc_iter % STAGES]);
         const bool trace_me = lane == 0 && (ew == 0 || ew == NUM_EPI_WARPS - 1);
         const int trow = gtrace_row(it, g, p.G);
         if (trace_me) gtrace(trow, ew == 0 ? 3 : 5);
@@ -437,7 +428,6 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           __syncwarp();
           if (lane == 0) ptx::mbar_arrive_cluster(b ? tempty_addr1 : tempty_addr0);
         }
-        if (RRS_GEMM_ONE_COMMIT == 2 && !kPlain && et == 0) ptx::mbar_arrive(&empty[acc_iter % STAGES]);
         ++acc_iter;
       }
       // ---- epilogue: Y = acc * beta_n  (acc already carries alpha_t * out_scale)
@@ -607,7 +597,9 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.T = (int)a.T;
   p.N = (int)a.N;
   p.K = (int)a.K;
-  p.G = (int)(a.K / BK);
+  p.G = (int)(a.K / a.group);
+  p.KB = (int)(a.K / BK);
+  p.gk = a.group / 32;
   p.num_m = (int)((a.T + BM * kCta - 1) / (BM * kCta));
   p.num_n = (int)((a.N + BN - 1) / BN);
   p.num_tiles = p.num_m * p.num_n;
@@ -634,7 +626,7 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
 cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {
   using namespace gemm;
   if (a.T <= 0) return cudaSuccess;
-  if (a.K / BK > MAX_G || a.K % BK) return cudaErrorInvalidValue;
+  if (a.group < 32 || a.group % 32 || a.K % a.group || a.K / a.group > MAX_G || a.K % BK) return cudaErrorInvalidValue;
   // CTA pairs (M = 256) once there are enough tokens to fill them; single CTAs for decode-sized T
   if (a.fp8) return a.T > BM ? launch_cta<2, true>(a, nsm, st) : launch_cta<1, true>(a, nsm, st);
   return a.T > BM ? launch_cta<2, false>(a, nsm, st) : launch_cta<1, false>(a, nsm, st);

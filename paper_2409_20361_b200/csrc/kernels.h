@@ -40,11 +40,11 @@ cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned
 bool prologue_fused_supports_k(int64_t K);
 cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
                                   unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                  float* scale, bool e4m3, int nsm, cudaStream_t st);
+                                  float* scale, bool e4m3, int group, int nsm, cudaStream_t st);
 // chan_max_bits == nullptr: weight mode (no smoothing, s_group unused)
 cudaError_t launch_smooth_quant(const float* Xr, int64_t T, int64_t K, const int32_t* perm,
                                 const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                float* scale, bool e4m3, int nsm, cudaStream_t st);
+                                float* scale, bool e4m3, int group, int nsm, cudaStream_t st);
 cudaError_t launch_perm_rank(const float* c, int64_t K, int32_t* perm, cudaStream_t st);
 
 struct GemmArgs {

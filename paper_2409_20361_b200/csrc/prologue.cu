@@ -196,15 +196,17 @@ RRS_DEVICE void load_perm32(const int32_t* __restrict__ perm, int j0, int (&pj)[
   }
 }
 
-// s_g = max_{j' in g} c[perm[j']] (the 4 consecutive threads of a 128-wide group) from chan_max staged
-// in shared memory; 0 -> 1 (R8); returns fl(1/s_g) (R9).  CTA 0's first tile row publishes s_group.
-RRS_DEVICE float group_inv_scale(const float* cms, const int (&pj)[32], int j0, bool publish, float* s_group_out) {
+// s_g = max_{j' in g} c[perm[j']] (the group/32 consecutive threads of a group -- 4 for the paper's 128,
+// P:189) from chan_max staged in shared memory; 0 -> 1 (R8); returns fl(1/s_g) (R9).  CTA 0's first tile row
+// publishes s_group.  group in {32, 64, ..., 1024}, a divisor of the row's thread count x 32.
+RRS_DEVICE float group_inv_scale(const float* cms, const int (&pj)[32], int j0, bool publish, float* s_group_out,
+                                 int group) {
   float m = 0.0f;
 #pragma unroll
   for (int k = 0; k < 32; ++k) m = fmaxf(m, cms[pj[k]]);
-  m = seg_max(m, 4);
+  m = seg_max(m, group >> 5);
   if (m == 0.0f) m = 1.0f;
-  if (publish && (j0 & 127) == 0 && s_group_out) s_group_out[j0 >> 7] = m;
+  if (publish && j0 % group == 0 && s_group_out) s_group_out[j0 / group] = m;
   return __frcp_rn(m);
 }
 
@@ -295,7 +297,7 @@ __global__ void __cluster_dims__(colmax_cluster<K>(), 1, 1) __launch_bounds__(Fw
 prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
                       float* __restrict__ Xr, unsigned* __restrict__ counter, const int32_t* __restrict__ perm,
                       float* __restrict__ s_group_out, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
-                      float* __restrict__ scale_out, int e4m3) {
+                      float* __restrict__ scale_out, int e4m3, int group) {
   using P = FwhtPlan<K>;
   using S = ColmaxSmem<K>;
   static_assert(P::kPow2 && P::E == 32, "fused prologue: 2^m plans (32 positions per thread in both passes)");
@@ -352,7 +354,7 @@ prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __res
   trace(1, 2);
   ptx::mbar_wait(&bar[2], 0);
   trace(1, 4);
-  const float inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out);
+  const float inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out, group);
   trace(1, 5);
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -386,7 +388,8 @@ template <int K>
 __global__ void __launch_bounds__(QuantPlan<K>::THREADS)
 smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __restrict__ perm,
                     const unsigned* __restrict__ chan_max_bits, float* __restrict__ s_group_out,
-                    uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out, int e4m3) {
+                    uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out, int e4m3,
+                    int group) {
   using Q = QuantPlan<K>;
   constexpr int TPR = Q::TPR;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -427,7 +430,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
     for (int c = tid * 4; c < K; c += Q::THREADS * 4)  // chan_max -> shared memory, coalesced
       *reinterpret_cast<uint4*>(cms + c) = __ldcg(reinterpret_cast<const uint4*>(chan_max_bits + c));
     __syncthreads();
-    inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out);
+    inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out, group);
   }
   trace(1, 2);
 
@@ -502,7 +505,7 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
 template <int K>
 static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, float* Xr, unsigned* counter,
                                   const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3,
-                                  int nsm, cudaStream_t st) {
+                                  int group, int nsm, cudaStream_t st) {
   using P = FwhtPlan<K>;
   auto kern = prologue_fused_kernel<K>;
   const int smem = ColmaxSmem<K>::BYTES;
@@ -522,13 +525,13 @@ static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, fl
   const int64_t tiles = (T + P::R - 1) / P::R;
   const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>()));
   const int grid = (int)clusters * colmax_cluster<K>();
-  kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr, counter, perm, s_group, Xq, Xq8, scale, (int)e4m3);
+  kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr, counter, perm, s_group, Xq, Xq8, scale, (int)e4m3, group);
   return cudaGetLastError();
 }
 
 template <int K>
 static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* perm, const unsigned* cm,
-                                  float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int nsm,
+                                  float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int group, int nsm,
                                   cudaStream_t st) {
   using Q = QuantPlan<K>;
   auto kern = smooth_quant_kernel<K>;
@@ -540,7 +543,7 @@ static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* per
     if (cm == nullptr || s_group == nullptr) return cudaSuccess;
     grid = 1;  // T == 0: still publish s_group (all ones, R8)
   }
-  return launch_pdl(kern, grid, Q::THREADS, Q::BYTES, st, Xr, T, perm, cm, s_group, Xq, Xq8, scale, (int)e4m3);
+  return launch_pdl(kern, grid, Q::THREADS, Q::BYTES, st, Xr, T, perm, cm, s_group, Xq, Xq8, scale, (int)e4m3, group);
 }
 
 #define RRS_FOR_EACH_K(M) M(128) M(256) M(512) M(1024) M(2048) M(4096) M(8192) M(16384) M(7168) M(14336)
@@ -551,9 +554,9 @@ bool prologue_fused_supports_k(int64_t K) { return K >= 128 && K <= 16384 && (K 
 
 cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
                                   unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                  float* scale, bool e4m3, int nsm, cudaStream_t st) {
+                                  float* scale, bool e4m3, int group, int nsm, cudaStream_t st) {
   switch (K) {
-#define RRS_CASE(k) case k: return launch_fused_k<k>(X, T, chan_max_bits, Xr, counter, perm, s_group, Xq, Xq8, scale, e4m3, nsm, st);
+#define RRS_CASE(k) case k: return launch_fused_k<k>(X, T, chan_max_bits, Xr, counter, perm, s_group, Xq, Xq8, scale, e4m3, group, nsm, st);
     RRS_FOR_EACH_POW2_K(RRS_CASE)
 #undef RRS_CASE
     default: return cudaErrorInvalidValue;
@@ -581,9 +584,9 @@ cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned
 
 cudaError_t launch_smooth_quant(const float* Xr, int64_t T, int64_t K, const int32_t* perm,
                                 const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                float* scale, bool e4m3, int nsm, cudaStream_t st) {
+                                float* scale, bool e4m3, int group, int nsm, cudaStream_t st) {
   switch (K) {
-#define RRS_CASE(k) case k: return launch_quant_k<k>(Xr, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, e4m3, nsm, st);
+#define RRS_CASE(k) case k: return launch_quant_k<k>(Xr, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, e4m3, group, nsm, st);
     RRS_FOR_EACH_K(RRS_CASE)
 #undef RRS_CASE
     default: return cudaErrorInvalidValue;

@@ -17,8 +17,8 @@ def dev_bf16(bits: np.ndarray, device="cuda") -> torch.Tensor:
     return t.to(device).view(torch.bfloat16)
 
 
-def oracle_layer(X_bits, W_bits, perm, keep_partials=True):
-    return o.rrs_linear(bf16_bits_to_f64(X_bits), bf16_bits_to_f64(W_bits), np.asarray(perm), L=128,
+def oracle_layer(X_bits, W_bits, perm, keep_partials=True, group=128):
+    return o.rrs_linear(bf16_bits_to_f64(X_bits), bf16_bits_to_f64(W_bits), np.asarray(perm), L=group,
                         keep_partials=keep_partials)
 
 

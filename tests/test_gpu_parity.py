@@ -35,20 +35,20 @@ def _u32(t):
     return t.cpu().numpy().view(np.uint32)
 
 
-def _run_prologue(X_bits, perm, i8=False):
+def _run_prologue(X_bits, perm, i8=False, group=128):
     T, K = X_bits.shape
     X = dev_bf16(X_bits)
     p = torch.from_numpy(perm).to(DEV)
     Xq = torch.empty((T, K // 2), dtype=torch.uint8, device=DEV)
     Xop = torch.empty((T, K), dtype=torch.uint8, device=DEV)
     xs = torch.empty(T, dtype=torch.float32, device=DEV)
-    sg = torch.empty(K // 128, dtype=torch.float32, device=DEV)
+    sg = torch.empty(K // group, dtype=torch.float32, device=DEV)
     cm = torch.empty(K, dtype=torch.float32, device=DEV)
-    rrs.rrs_rotate_smooth_quant(X, p, Xq, Xop, xs, sg, chan_max=cm, i8=i8)
+    rrs.rrs_rotate_smooth_quant(X, p, Xq, Xop, xs, sg, chan_max=cm, group=group, i8=i8)
     # the operand-only call (Xq = NULL) is the rrs_linear hot path, which takes a separate code path in the
     # quantisation kernel: its bytes must be identical
     Xop2 = torch.empty_like(Xop)
-    rrs.rrs_rotate_smooth_quant(X, p, None, Xop2, torch.empty_like(xs), torch.empty_like(sg), i8=i8)
+    rrs.rrs_rotate_smooth_quant(X, p, None, Xop2, torch.empty_like(xs), torch.empty_like(sg), group=group, i8=i8)
     torch.cuda.synchronize()
     assert torch.equal(Xop, Xop2)
     return dict(Xq=Xq.cpu().numpy(), Xop=Xop.cpu().numpy(), Xq8=decode_operand(Xop.cpu().numpy(), i8),
@@ -99,6 +99,24 @@ def test_prologue_bitexact(K, T, profile, i8):
     assert np.array_equal(g["alpha"].view(np.uint32), a.view(np.uint32))
     assert np.array_equal(g["Xq8"], q)
     assert np.array_equal(g["Xop"], encode_operand(q, i8))  # every operand byte
+    assert np.array_equal(g["Xq"], o.pack_int4(q))
+
+
+@pytest.mark.parametrize("K,T,profile,group", [(1024, 70, "channel", 32), (4096, 129, "spike", 64),
+                                               (4096, 40, "mixed", 256), (14336, 24, "channel", 512),
+                                               (2048, 9, "channel", 1024), (256, 300, "channel", 32)])
+def test_prologue_group_variants_bitexact(K, T, profile, group):
+    """SURVEY §8 f3 / Table 4: the smoothing group is a parameter (P:189 picks 128)."""
+    X_bits = make_activations(profile, T, K, 313, 414)
+    perm = _perm(make_activations(profile, 64, K, 313, 415))
+    g = _run_prologue(X_bits, perm, group=group)
+    Xr = o.rotate(bf16_bits_to_f64(X_bits))
+    s = o.group_scales(o.channel_max(Xr), perm, group)
+    q, a = o.smooth_quant(Xr, perm, s, group)
+    assert g["s_group"].shape == (K // group,)
+    assert np.array_equal(g["s_group"].view(np.uint32), s.view(np.uint32))
+    assert np.array_equal(g["alpha"].view(np.uint32), a.view(np.uint32))
+    assert np.array_equal(g["Xq8"], q)
     assert np.array_equal(g["Xq"], o.pack_int4(q))
 
 
@@ -156,6 +174,22 @@ def test_group_partials_bitexact(T, N, K, i8):
     rrs.rrs_debug_group_partials(_dev(encode_operand(q, i8)), _dev(encode_operand(qw, i8)), P, i8=i8)
     torch.cuda.synchronize()
     assert np.array_equal(P.cpu().numpy(), o.group_partials(q, qw, 128))
+
+
+@pytest.mark.parametrize("T,N,K,group", [(300, 600, 512, 32), (129, 257, 1024, 64), (520, 488, 2048, 256),
+                                         (64, 240, 4096, 512), (8, 256, 1024, 1024)])
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_group_partials_group_variants_bitexact(T, N, K, group, i8):
+    """Per-group partials for groups smaller than (closed inside) and larger than (spanning) a 128-deep K-block."""
+    rng = np.random.default_rng(T * 11 + group)
+    q = rng.integers(-7, 8, size=(T, K)).astype(np.int8)
+    qw = rng.integers(-7, 8, size=(N, K)).astype(np.int8)
+    q[0, :] = 7
+    qw[0, :] = -7  # |P_g| = 49 * group, the extreme
+    P = torch.empty((K // group, T, N), dtype=torch.int32, device=DEV)
+    rrs.rrs_debug_group_partials(_dev(encode_operand(q, i8)), _dev(encode_operand(qw, i8)), P, group=group, i8=i8)
+    torch.cuda.synchronize()
+    assert np.array_equal(P.cpu().numpy(), o.group_partials(q, qw, group))
 
 
 def _gemm_case(T, N, K, profile="channel", seed=0):
@@ -230,6 +264,22 @@ def test_rrs_linear_end_to_end(wl, T, N, i8):
     assert torch.equal(Yb, Y.to(torch.bfloat16))  # RNE of the same f32 accumulation
 
 
+@pytest.mark.parametrize("T,N,K,group,i8", [(257, 520, 4096, 32, False), (130, 264, 4096, 64, True),
+                                            (300, 264, 14336, 256, False), (129, 240, 8192, 512, False),
+                                            (64, 256, 2048, 1024, True)])
+def test_rrs_linear_group_variants(T, N, K, group, i8):
+    """Whole layer at the Table-4 group sizes: codes from the same seeded LLaMA-like inputs,
+    Y within the DESIGN.md §5 tolerance of the oracle run with the same group."""
+    X_bits = make_activations("mixed", T, K, 930, 931)
+    W_bits = make_weights(N, K, 932)
+    perm = _perm(make_activations("mixed", 64, K, 930, 933))
+    ref = oracle_layer(X_bits, W_bits, perm, group=group)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), i8=i8, group=group)
+    Y = layer(dev_bf16(X_bits), out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
+
+
 def test_rrs_linear_equals_prologue_plus_gemm_bitwise():
     X_bits, W_bits, perm, ref = _gemm_case(200, 512, 4096)
     X = dev_bf16(X_bits)
@@ -299,8 +349,11 @@ def test_invalid_arguments_raise():
     xs = torch.empty(4, device=DEV)
     sg = torch.empty(2, device=DEV)
     with pytest.raises(rrs.RRSError) as e:
-        rrs.rrs_rotate_smooth_quant(X, p, None, None, xs, sg, chan_max=torch.empty(256, device=DEV), group=64)
-    assert e.value.status == 1
+        rrs.rrs_rotate_smooth_quant(X, p, None, None, xs, sg, chan_max=torch.empty(256, device=DEV), group=48)
+    assert e.value.status == 1  # not a power of two
+    with pytest.raises(rrs.RRSError) as e:
+        rrs.rrs_rotate_smooth_quant(X, p, None, None, xs, sg, chan_max=torch.empty(256, device=DEV), group=2048)
+    assert e.value.status == 1  # above 1024
     Xbad = torch.zeros((4, 96 * 3), dtype=torch.bfloat16, device=DEV)
     with pytest.raises(rrs.RRSError) as e:
         rrs.rrs_rotate_smooth_quant(Xbad, p, None, None, xs, sg, chan_max=torch.empty(288, device=DEV))
