@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <vector>
 #include <algorithm>
+#include <cstdlib>
 #include "../../paper_2409_20361_b200/csrc/gemm.cu"
 
 int main(int argc, char** argv) {
@@ -13,14 +14,17 @@ int main(int argc, char** argv) {
   cudaMalloc(&X, TM * KM); cudaMalloc(&W, NM * KM); cudaMalloc(&xs, TM * 4); cudaMalloc(&sg, KM / 128 * 4);
   cudaMalloc(&ws, NM * 4); cudaMalloc(&Y, TM * NM * 2);
   cudaMemset(X, 0x38, TM * KM); cudaMemset(W, 0x38, NM * KM);
-  std::vector<float> one(NM, 1.0f);
+  std::vector<float> one(TM > NM ? TM : NM, 1.0f);
   cudaMemcpy(xs, one.data(), TM * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(ws, one.data(), NM * 4, cudaMemcpyHostToDevice);
-  cudaMemcpy(sg, one.data(), KM / 128 * 4, cudaMemcpyHostToDevice);
+  cudaFree(sg);
+  cudaMalloc(&sg, KM / 32 * 4);
+  cudaMemcpy(sg, one.data(), KM / 32 * 4, cudaMemcpyHostToDevice);
   for (int a0 = 1; a0 + 3 < argc; a0 += 4) {
     const int64_t T = atoll(argv[a0]), N = atoll(argv[a0 + 1]), K = atoll(argv[a0 + 2]);
     const int plain = atoi(argv[a0 + 3]);
-    rrs::GemmArgs a{X, xs, sg, W, ws, T, N, K, 128, 1.0f / K, plain != 0, true, Y, 0, N, nullptr};
+    const int group = getenv("RRS_GROUP") ? atoi(getenv("RRS_GROUP")) : 128;
+    rrs::GemmArgs a{X, xs, sg, W, ws, T, N, K, group, 1.0f / K, plain != 0, true, Y, 0, N, nullptr};
     std::vector<float> v;
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);

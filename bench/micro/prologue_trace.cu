@@ -33,7 +33,7 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    rrs::launch_prologue_fused(X, T, K, cm, Xr, counter, perm, sg, nullptr, q, sc, true, nsm, 0);
+    rrs::launch_prologue_fused(X, T, K, cm, Xr, counter, perm, sg, nullptr, q, sc, true, 128, nsm, 0);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float a;
@@ -47,7 +47,7 @@ int main(int argc, char** argv) {
     cudaEventRecord(e0);
     rrs::launch_fwht_colmax(X, T, K, cm, Xr, nsm, 0);
     cudaEventRecord(e1);
-    rrs::launch_smooth_quant(Xr, T, K, perm, cm, sg, nullptr, q, sc, true, nsm, 0);
+    rrs::launch_smooth_quant(Xr, T, K, perm, cm, sg, nullptr, q, sc, true, 128, nsm, 0);
     cudaEventRecord(e2);
     cudaError_t e = cudaDeviceSynchronize();
     float a, b;

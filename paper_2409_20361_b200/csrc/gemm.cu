@@ -202,61 +202,91 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     uint32_t acc_iter = 0;  // number of accumulator buffers filled so far
     int it = 0;             // local tile counter (timeline only)
     const uint64_t a_desc0 = ptx::smem_desc_sw128(sA), b_desc0 = ptx::smem_desc_sw128(sB);
-    // smoothing groups of gk = group / 32 MMA K-steps (4 for the paper's 128 = one K-block; the other
-    // Table-4 sizes close a group inside a K-block (32, 64) or after several (256+))
+    // smoothing groups of gk = group / 32 MMA K-steps: 4 for the paper's 128 = one K-block; the other
+    // Table-4 sizes span several K-blocks (256+) or close inside one (32, 64)
     const int gk = p.gk;
-    int ks = 0;  // K-steps of the current group issued so far
-    for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
-      for (int kb = 0; kb < p.KB; ++kb, it += (kb == p.KB)) {
-        const int trow = gtrace_row(it, kb, p.KB);
-        gtrace(trow, 0);
-        if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&full[stage], phase);
-        else ptx::mbar_wait(&full[stage], phase);
-        gtrace(trow, 1);
-        ptx::tc_fence_after();
-        // descriptor start addresses advance in 16-byte units: stage offsets, then 32 bytes per K step
-        const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
-        const uint64_t b_desc = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
-#pragma unroll
-        for (int k = 0; k < BK / 32; ++k) {
+    auto wait_tempty = [&](uint32_t b) {
+      // a new accumulation into buffer b: use u = acc_iter >> 1 of it needs the u-th release (completion #u
+      // of tempty[b]); the releases come from both CTAs of a pair (cluster-scope acquire for int8)
+      if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
+      else if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
+      else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
+    };
+    auto wait_full = [&]() {
+      if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&full[stage], phase);
+      else ptx::mbar_wait(&full[stage], phase);
+      ptx::tc_fence_after();
+    };
+    auto mma = [&](uint32_t d, uint64_t a_desc, uint64_t b_desc, int k, uint32_t acc) {
+      // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier: always
+      // accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
+      if constexpr (kFp8) {
+        if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
+        else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
+      } else {
+        if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
+        else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
+      }
+    };
+    auto commit = [&](uint64_t* bar) {
+      if constexpr (kCta == 1) ptx::mma_commit(bar);
+      else ptx::mma_commit_pair(bar, 0x3);
+    };
+    if (kPlain || gk >= 4) {
+      // whole K-blocks per group (the hot path): 4 MMAs back to back per K-block
+      const int gpb = kPlain ? p.KB : gk / 4;  // K-blocks per accumulation
+      for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
+        int kin = 0;  // K-blocks into the current accumulation
+        for (int kb = 0; kb < p.KB; ++kb, it += (kb == p.KB)) {
+          const int trow = gtrace_row(it, kb, p.KB);
           const uint32_t b = acc_iter & 1;
-          if (kPlain ? (kb == 0 && k == 0) : ks == 0) {
-            // a new accumulation into buffer b: use u = acc_iter >> 1 of it needs the u-th release (completion
-            // #u of tempty[b]); the releases come from both CTAs of a pair (cluster-scope acquire for int8)
-            if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
-            else if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
-            else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
-            ptx::tc_fence_after();
-          }
+          if (kin == 0) wait_tempty(b);
+          gtrace(trow, 0);
+          wait_full();
+          gtrace(trow, 1);
+          // descriptor start addresses advance in 16-byte units: stage offsets, then 32 bytes per K step
+          const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
+          const uint64_t b_desc = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
           const uint32_t d = tmem_base + b * ACC_STRIDE;
-          // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier:
-          // always accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
-          if constexpr (kFp8) {
-            const uint32_t acc = kPlain ? (kb > 0 || k > 0) : (ks > 0);
-            if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
-            else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
-          } else {
-            if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
-            else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
-          }
-          if (!kPlain && ++ks == gk) {  // group complete: hand the buffer to the promotion warps
-            if constexpr (kCta == 1) ptx::mma_commit(&tfull[b]);
-            else ptx::mma_commit_pair(&tfull[b], 0x3);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k) mma(d, a_desc, b_desc, k, (kin > 0 || k > 0) ? 1u : 0u);
+          // the SMEM stage is free once these MMAs complete (a second commit per group costs ~18 ns of
+          // tensor-pipe time, but freeing the stage from a promotion thread instead was slower)
+          commit(&empty[stage]);
+          if (++kin == gpb) {  // accumulation complete: hand the buffer to the promotion warps
+            commit(&tfull[b]);
             ++acc_iter;
-            ks = 0;
+            kin = 0;
           }
+          gtrace(trow, 2);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        // the SMEM stage is free once these MMAs complete (a second commit per group costs ~18 ns of
-        // tensor-pipe time, but freeing the stage from a promotion thread instead was slower)
-        if constexpr (kCta == 1) ptx::mma_commit(&empty[stage]);
-        else ptx::mma_commit_pair(&empty[stage], 0x3);
-        if (kPlain && kb == p.KB - 1) {
-          if constexpr (kCta == 1) ptx::mma_commit(&tfull[acc_iter & 1]);
-          else ptx::mma_commit_pair(&tfull[acc_iter & 1], 0x3);
-          ++acc_iter;
+      }
+    } else {
+      // groups of 32 or 64 codes: gk = 1 or 2 MMA K-steps, several groups per K-block
+      int ks = 0;  // K-steps of the current group issued so far
+      for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
+        for (int kb = 0; kb < p.KB; ++kb) {
+          wait_full();
+          const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
+          const uint64_t b_desc = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
+#pragma unroll
+          for (int k = 0; k < BK / 32; ++k) {
+            const uint32_t b = acc_iter & 1;
+            if (ks == 0) {
+              wait_tempty(b);
+              ptx::tc_fence_after();
+            }
+            mma(tmem_base + b * ACC_STRIDE, a_desc, b_desc, k, ks > 0 ? 1u : 0u);
+            if (++ks == gk) {
+              commit(&tfull[b]);
+              ++acc_iter;
+              ks = 0;
+            }
+          }
+          commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        gtrace(trow, 2);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
     }
     __syncwarp();
