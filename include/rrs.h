@@ -62,6 +62,7 @@ typedef enum { RRS_BF16 = 0, RRS_F32 = 1 } rrs_dtype;
 /* flags */
 #define RRS_GEMM_PLAIN 0x1u   /* rrs_gemm: per-channel A4W4 baseline: one sum over all K, no s_g */
 #define RRS_OPERAND_I8 0x2u   /* GEMM operands are int8 codes (tcgen05 .kind::i8) instead of E4M3 bytes */
+#define RRS_TOKEN_SHARDED 0x4u /* rrs_linear with comm: token-sharded data parallel, see below */
 
 typedef struct rrs_comm_s* rrs_comm_t;
 
@@ -129,7 +130,14 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
  * comm == NULL: single GPU, Wop/w_scale hold all N rows.
  * comm != NULL (column-parallel): Wop/w_scale hold THIS rank's N/world output rows
  *   [rank*N/world, (rank+1)*N/world); X is replicated; every rank runs the identical prologue; Y
- *   receives all N columns through an NCCL all-gather.  N_total % world == 0 required. */
+ *   receives all N columns through an NCCL all-gather.  N_total % world == 0 required.
+ * comm != NULL and flags & RRS_TOKEN_SHARDED (data parallel over tokens): X holds THIS
+ *   rank's T tokens (T may differ between ranks, 0 included), Wop/w_scale hold all N_total rows, Y
+ *   receives this rank's [T][N_total].  The runtime channel max is over ALL tokens of the call (Eq. 1
+ *   P:90, R6): the rotate pass writes chan_max of the local tokens, one ncclAllReduce(MAX) of chan_max[K]
+ *   f32 combines them, then every rank smooths and quantises with the same s_g -- codes, alpha_t and Y rows
+ *   are bit-identical to one call on the concatenated tokens.  No output collective.  Every rank of comm
+ *   must call it (collective). */
 rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
                       const int32_t* perm, const uint8_t* Wop, const float* w_scale, int64_t N_total,
                       void* Y, int32_t y_dtype, int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes,

@@ -41,12 +41,16 @@ class RRSLinear:
     """Y = RRS-A4W4(X) @ W^T for a bf16 nn.Linear weight W[N][K] (column shard when comm is given)."""
 
     def __init__(self, W: torch.Tensor, perm: torch.Tensor, comm=None, world: int = 1, rank: int = 0,
-                 keep_packed: bool = False, i8: bool = False, group: int = GROUP, stream=None):
+                 keep_packed: bool = False, i8: bool = False, group: int = GROUP, token_sharded: bool = False,
+                 stream=None):
+        """token_sharded: data parallel over tokens -- every rank keeps all N rows of W, calls
+        with its own token slab and gets its own rows of Y; one all-reduce(MAX) of chan_max per call."""
         N, K = W.shape
         self.group = group  # smoothing group (P:189: 128; SURVEY §8 f3: any power of two in [32, 1024])
         self.K, self.N_total = K, N
         self.comm, self.world, self.rank = comm, world, rank
-        lo, hi = shard_rows(N, world, rank)
+        self.token_sharded = token_sharded
+        lo, hi = (0, N) if token_sharded else shard_rows(N, world, rank)
         Wl = W[lo:hi].contiguous()
         dev = W.device
         self.perm = perm.to(device=dev, dtype=torch.int32).contiguous()
@@ -58,7 +62,7 @@ class RRSLinear:
         self._ws = None
 
     def workspace(self, T: int, device) -> torch.Tensor:
-        need = rrs_workspace_bytes(T, self.N_total, self.K, self.group, self.world)
+        need = rrs_workspace_bytes(T, self.N_total, self.K, self.group, 1 if self.token_sharded else self.world)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=device)
         return self._ws
@@ -68,7 +72,7 @@ class RRSLinear:
         if Y is None:
             Y = torch.empty((T, self.N_total), dtype=out_dtype, device=X.device)
         rrs_linear(X, self.perm, self.Wop, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
-                   comm=self.comm, group=self.group, i8=self.i8, stream=stream)
+                   comm=self.comm, group=self.group, i8=self.i8, token_sharded=self.token_sharded, stream=stream)
         return Y
 
 

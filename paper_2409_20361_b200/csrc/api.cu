@@ -312,6 +312,39 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
 }
 
+// token-sharded data parallel.  The prologue runs as its two passes (the fused single-kernel
+// prologue has a grid barrier where the cross-rank reduction must go): rotate + local channel max, one
+// ncclAllReduce(MAX) of chan_max[K] (non-negative floats: max is exact and order-free), smooth + quantise.
+static rrs_status linear_token_sharded(const void* X, int64_t T, int64_t K, int32_t group, const int32_t* perm,
+                                       const int8_t* Wq8, const float* w_scale, int64_t N, void* Y, int32_t y_dtype,
+                                       int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, bool e4m3, int nsm,
+                                       cudaStream_t st) {
+  if (N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "N_total=%lld < 1", (long long)N);
+  if ((T > 0 && !X) || !perm) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
+  Workspace w;
+  const size_t need = carve(ws, T, N, K, group, 1, &w);
+  if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
+  if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
+  if (T > 0)
+    if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N, K, group, Y, ldy)) return s;
+  cudaError_t e = cudaMemsetAsync(w.chan_max, 0, sizeof(float) * K, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
+  e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(w.chan_max), w.Xr,
+                              nsm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "fwht_colmax_kernel");
+  ncclResult_t r = ncclAllReduce(w.chan_max, w.chan_max, (size_t)K, ncclFloat, ncclMax, comm->nccl, st);
+  if (r != ncclSuccess) return fail(RRS_ERR_NCCL, "ncclAllReduce(chan_max, MAX): %s", ncclGetErrorString(r));
+  if (T == 0) return RRS_OK;
+  e = rrs::launch_smooth_quant(w.Xr, T, K, perm, reinterpret_cast<const unsigned*>(w.chan_max), w.s_group, nullptr,
+                               w.Xq8, w.x_scale, e4m3, group, nsm, st);
+  if (e != cudaSuccess) return cuda_fail(e, "smooth_quant_kernel");
+  rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N, K, group, 1.0f / (float)K, false, e4m3, Y,
+                  y_dtype, ldy, nullptr};
+  e = rrs::launch_gemm(a, nsm, st);
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
+}
+
 rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group, const int32_t* perm,
                       const uint8_t* Wop, const float* w_scale, int64_t N_total, void* Y, int32_t y_dtype,
                       int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, uint32_t flags, void* stream) {
@@ -322,6 +355,9 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (rrs_status s = check_arch(nsm)) return s;
   if (x_dtype != RRS_BF16) return fail(RRS_ERR_INVALID_ARGUMENT, "X must be bf16 (R17)");
   if (rrs_status s = check_shape(T, K, group)) return s;
+  if (comm && (flags & RRS_TOKEN_SHARDED))
+    return linear_token_sharded(X, T, K, group, perm, Wq8, w_scale, N_total, Y, y_dtype, ldy, comm, ws, ws_bytes, e4m3,
+                                nsm, static_cast<cudaStream_t>(stream));
   const int world = comm ? comm->world : 1;
   if (N_total < 1 || N_total % world)
     return fail(RRS_ERR_INVALID_ARGUMENT, "N_total=%lld must be a positive multiple of world=%d", (long long)N_total, world);

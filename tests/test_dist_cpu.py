@@ -66,6 +66,21 @@ def _worker(rank, world, port, q):
         out["gathered"] = Y
         out["prologue"] = (mine["s_group"].tobytes(), mine["alpha"].tobytes(), mine["Xq"].tobytes())
 
+        # 5. token-sharded data parallel: each rank rotates its own token slab, the channel
+        #    maxima are combined by an all-reduce(MAX) (the only exchange), then each rank smooths, quantises
+        #    and multiplies its own tokens against all of W
+        T = 40
+        lo_t, hi_t = rank * T // world, (rank + 1) * T // world
+        Xr = o.rotate(X[lo_t:hi_t])
+        c = torch.from_numpy(o.channel_max(Xr).copy())
+        dist.all_reduce(c, op=dist.ReduceOp.MAX)
+        c = c.numpy()
+        s = o.group_scales(c, perm, 128)
+        codes, alpha = o.smooth_quant(Xr, perm, s, 128)
+        qw, beta, _ = o.prepare_weights(W, perm)
+        Yt = o.scale_accumulate_rows(codes, qw, s, alpha, beta, 128, 1.0 / X.shape[1])
+        out["dp"] = dict(rows=(lo_t, hi_t), chan_max=c, s=s, q=codes, alpha=alpha, Y=Yt)
+
         # 4. bench timing reduction
         out["max"] = bench.max_over_ranks([1.0 + rank, 3.0 + rank], torch.device("cpu"), world)
         q.put((rank, out))
@@ -115,3 +130,24 @@ def test_sharded_equals_unsharded_bitwise(dist_results):
 
 def test_max_over_ranks(dist_results):
     assert dist_results[0]["max"] == dist_results[1]["max"] == 3.0
+
+
+def test_token_sharded_equals_unsharded_bitwise(dist_results):
+    """all-reduce(MAX) of the per-rank channel maxima reproduces the call-wide maximum of Eq. 1
+    (R6), so s_g, every code, alpha_t and every Y row equal the single call on all tokens."""
+    from oracle import rrs_oracle as o
+    from rrs_synth import WORKLOADS, bf16_bits_to_f64, make_layer
+    w = WORKLOADS["c2_llama2_7b_qo"]
+    X_bits, W_bits, Xc = make_layer(w, T=40, N=520, T_cal=64)
+    perm = o.calibrate_perm(bf16_bits_to_f64(Xc))
+    full = o.rrs_linear(bf16_bits_to_f64(X_bits), bf16_bits_to_f64(W_bits), perm, L=128, keep_partials=False)
+    for r in dist_results.values():
+        d = r["dp"]
+        lo, hi = d["rows"]
+        assert np.array_equal(d["chan_max"].view(np.uint32), full["chan_max"].view(np.uint32))
+        assert np.array_equal(d["s"].view(np.uint32), full["s_group"].view(np.uint32))
+        assert np.array_equal(d["q"], full["q"][lo:hi])
+        assert np.array_equal(d["alpha"].view(np.uint32), full["alpha"][lo:hi].view(np.uint32))
+        assert np.array_equal(d["Y"], full["Y"][lo:hi])
+    spans = sorted(r["dp"]["rows"] for r in dist_results.values())
+    assert spans == [(0, 20), (20, 40)]

@@ -326,6 +326,32 @@ def test_comm_world1_path_equals_single_gpu():
         rrs.rrs_comm_destroy(comm)
 
 
+@pytest.mark.parametrize("K,T", [(4096, 200), (14336, 70), (1024, 0)])
+def test_token_sharded_world1_equals_single_gpu(K, T):
+    """Token-sharded data parallel (RRS_TOKEN_SHARDED) with a 1-rank communicator: the two-pass
+    prologue + ncclAllReduce(MAX) of chan_max + GEMM equals the single-GPU layer (fused prologue for 2^m)
+    bit for bit; T = 0 still joins the collective."""
+    X_bits = make_activations("mixed", T, K, 940, 941)
+    W_bits = make_weights(264, K, 942)
+    perm = _perm(make_activations("mixed", 64, K, 940, 943))
+    uid = rrs.rrs_comm_unique_id()
+    comm = rrs.rrs_comm_init(0, 1, uid)
+    try:
+        p = torch.from_numpy(perm).to(DEV)
+        single = rrs.RRSLinear(dev_bf16(W_bits), p)
+        dp = rrs.RRSLinear(dev_bf16(W_bits), p, comm=comm, world=1, rank=0, token_sharded=True)
+        X = dev_bf16(X_bits)
+        a = single(X, out_dtype=torch.float32)
+        b = dp(X, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert b.shape == (T, 264) and torch.equal(a, b)
+        if T:
+            ref = oracle_layer(X_bits, W_bits, perm)
+            assert y_normalised_error(b.cpu().numpy(), ref) <= 1e-5
+    finally:
+        rrs.rrs_comm_destroy(comm)
+
+
 def test_perm_helper_matches_oracle():
     K = 4096
     Xc = make_activations("channel", 64, K, 11, 12)
