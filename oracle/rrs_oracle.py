@@ -306,6 +306,15 @@ def bf16_round(y: np.ndarray) -> np.ndarray:
 # ----------------------------------------------------------------------------------------
 
 
+def swiglu(g: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """LLaMA MLP gate (the paper applies RRS to the up/gate and down_proj inputs of this block,
+    P:138): h = silu(g) * u = g / (1 + exp(-g)) * u, in float64 (the definition, written out)."""
+    g = np.asarray(g, dtype=np.float64)
+    u = np.asarray(u, dtype=np.float64)
+    with np.errstate(over="ignore"):
+        return g / (1.0 + np.exp(-g)) * u
+
+
 def calibrate_perm(X_cal: np.ndarray, rotate_x: bool = True) -> np.ndarray:
     """Offline reorder from calibration activations (R5): rotate -> channel max -> sort."""
     Xr = rotate(X_cal) if rotate_x else np.asarray(X_cal, dtype=F32)

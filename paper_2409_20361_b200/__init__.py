@@ -42,7 +42,7 @@ class RRSLinear:
 
     def __init__(self, W: torch.Tensor, perm: torch.Tensor, comm=None, world: int = 1, rank: int = 0,
                  keep_packed: bool = False, i8: bool = False, group: int = GROUP, token_sharded: bool = False,
-                 stream=None):
+                 swiglu: bool = False, stream=None):
         """token_sharded: data parallel over tokens -- every rank keeps all N rows of W, calls
         with its own token slab and gets its own rows of Y; one all-reduce(MAX) of chan_max per call."""
         N, K = W.shape
@@ -50,6 +50,7 @@ class RRSLinear:
         self.K, self.N_total = K, N
         self.comm, self.world, self.rank = comm, world, rank
         self.token_sharded = token_sharded
+        self.swiglu = swiglu  # rows are interleaved (gate_i, up_i) pairs; output = silu(gate) * up, N/2 columns
         lo, hi = (0, N) if token_sharded else shard_rows(N, world, rank)
         Wl = W[lo:hi].contiguous()
         dev = W.device
@@ -70,10 +71,35 @@ class RRSLinear:
     def __call__(self, X: torch.Tensor, out_dtype=torch.bfloat16, Y: torch.Tensor | None = None, stream=None):
         T = X.shape[0]
         if Y is None:
-            Y = torch.empty((T, self.N_total), dtype=out_dtype, device=X.device)
+            Y = torch.empty((T, self.N_total // (2 if self.swiglu else 1)), dtype=out_dtype, device=X.device)
         rrs_linear(X, self.perm, self.Wop, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
-                   comm=self.comm, group=self.group, i8=self.i8, token_sharded=self.token_sharded, stream=stream)
+                   comm=self.comm, group=self.group, i8=self.i8, token_sharded=self.token_sharded,
+                   swiglu=self.swiglu, stream=stream)
         return Y
+
+
+def interleave_gate_up(W_gate: torch.Tensor, W_up: torch.Tensor) -> torch.Tensor:
+    """[F][K] gate and up weights -> [2F][K] with row 2i = gate_i, row 2i+1 = up_i (RRS_GEMM_SWIGLU layout)."""
+    if W_gate.shape != W_up.shape:
+        raise ValueError("gate / up shapes differ")
+    return torch.stack([W_gate, W_up], dim=1).reshape(2 * W_gate.shape[0], W_gate.shape[1]).contiguous()
+
+
+class RRSMLP:
+    """LLaMA MLP block with RRS A4W4 linears (P:138 applies RRS to the up/gate and the down_proj
+    inputs, where the paper places online rotation):
+        h = silu(X W_gate^T) * (X W_up^T)   -- ONE prologue on X and ONE GEMM over the interleaved 2F rows,
+                                               SwiGLU fused into the GEMM epilogue (bf16 h written once)
+        Y = RRS(h) W_down^T                 -- the down_proj RRS layer (K = F, e.g. 14336 = 28 * 512)
+    perm_in / perm_mid: offline reorders of X and of h (calibrate_perm on calibration activations)."""
+
+    def __init__(self, W_gate, W_up, W_down, perm_in, perm_mid, i8: bool = False, stream=None):
+        self.up_gate = RRSLinear(interleave_gate_up(W_gate, W_up), perm_in, i8=i8, swiglu=True, stream=stream)
+        self.down = RRSLinear(W_down, perm_mid, i8=i8, stream=stream)
+
+    def __call__(self, X: torch.Tensor, out_dtype=torch.bfloat16, stream=None):
+        h = self.up_gate(X, out_dtype=torch.bfloat16, stream=stream)
+        return self.down(h, out_dtype=out_dtype, stream=stream)
 
 
 def broadcast_unique_id(group=None) -> bytes:

@@ -282,12 +282,15 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
 }
 
 static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int8_t* Wq8, const float* w_scale,
-                              int64_t T, int64_t N, int64_t K, int32_t group, const void* Y, int64_t ldy) {
+                              int64_t T, int64_t N, int64_t K, int32_t group, const void* Y, int64_t ldy,
+                              bool swiglu = false) {
+  if (swiglu && N % 2) return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_GEMM_SWIGLU needs an even N (gate/up pairs)");
+  const int64_t n_out = swiglu ? N / 2 : N;
   if (T < 0 || N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "T=%lld N=%lld", (long long)T, (long long)N);
   if (rrs_status s = check_group(K, group)) return s;
   if (T > 0 && (!Xq8 || !x_scale || !Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (!Wq8 || !w_scale) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
-  if (ldy < N) return fail(RRS_ERR_INVALID_ARGUMENT, "ldy=%lld < N=%lld", (long long)ldy, (long long)N);
+  if (ldy < n_out) return fail(RRS_ERR_INVALID_ARGUMENT, "ldy=%lld < %lld output columns", (long long)ldy, (long long)n_out);
   if (!aligned16(Xq8) || !aligned16(Wq8) || !aligned16(Y) || ldy % 8)
     return fail(RRS_ERR_MISALIGNED, "pointers 16-byte aligned and ldy %% 8 == 0 required");
   return RRS_OK;
@@ -301,13 +304,16 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
   g_last_error.clear();
   int nsm;
   if (rrs_status s = check_arch(nsm)) return s;
-  if (rrs_status s = gemm_checks(Xq8, x_scale, Wq8, w_scale, T, N, K, group, Y, ldy)) return s;
+  const bool swiglu = (flags & RRS_GEMM_SWIGLU) != 0;
+  if (rrs_status s = gemm_checks(Xq8, x_scale, Wq8, w_scale, T, N, K, group, Y, ldy, swiglu)) return s;
   const bool plain = (flags & RRS_GEMM_PLAIN) != 0;
+  if (swiglu && (plain || y_dtype != RRS_BF16))
+    return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_GEMM_SWIGLU: bf16 output of the RRS (not plain) GEMM only");
   if (!plain && !s_group) return fail(RRS_ERR_INVALID_ARGUMENT, "s_group is NULL");
   if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
   if (T == 0) return RRS_OK;
   rrs::GemmArgs a{Xq8, x_scale, s_group, Wq8, w_scale, T, N, K, group, out_scale, plain,
-                  (flags & RRS_OPERAND_I8) == 0, Y, y_dtype, ldy, nullptr};
+                  (flags & RRS_OPERAND_I8) == 0, Y, y_dtype, ldy, nullptr, swiglu};
   cudaError_t e = rrs::launch_gemm(a, nsm, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
 }
@@ -317,8 +323,8 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
 // ncclAllReduce(MAX) of chan_max[K] (non-negative floats: max is exact and order-free), smooth + quantise.
 static rrs_status linear_token_sharded(const void* X, int64_t T, int64_t K, int32_t group, const int32_t* perm,
                                        const int8_t* Wq8, const float* w_scale, int64_t N, void* Y, int32_t y_dtype,
-                                       int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, bool e4m3, int nsm,
-                                       cudaStream_t st) {
+                                       int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, bool e4m3,
+                                       bool swiglu, int nsm, cudaStream_t st) {
   if (N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "N_total=%lld < 1", (long long)N);
   if ((T > 0 && !X) || !perm) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
@@ -327,7 +333,7 @@ static rrs_status linear_token_sharded(const void* X, int64_t T, int64_t K, int3
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   if (T > 0)
-    if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N, K, group, Y, ldy)) return s;
+    if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N, K, group, Y, ldy, swiglu)) return s;
   cudaError_t e = cudaMemsetAsync(w.chan_max, 0, sizeof(float) * K, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
   e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(w.chan_max), w.Xr,
@@ -340,7 +346,7 @@ static rrs_status linear_token_sharded(const void* X, int64_t T, int64_t K, int3
                                w.Xq8, w.x_scale, e4m3, group, nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "smooth_quant_kernel");
   rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N, K, group, 1.0f / (float)K, false, e4m3, Y,
-                  y_dtype, ldy, nullptr};
+                  y_dtype, ldy, nullptr, swiglu};
   e = rrs::launch_gemm(a, nsm, st);
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
 }
@@ -355,9 +361,11 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (rrs_status s = check_arch(nsm)) return s;
   if (x_dtype != RRS_BF16) return fail(RRS_ERR_INVALID_ARGUMENT, "X must be bf16 (R17)");
   if (rrs_status s = check_shape(T, K, group)) return s;
+  const bool swiglu = (flags & RRS_GEMM_SWIGLU) != 0;
+  if (swiglu && y_dtype != RRS_BF16) return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_GEMM_SWIGLU: bf16 output only");
   if (comm && (flags & RRS_TOKEN_SHARDED))
     return linear_token_sharded(X, T, K, group, perm, Wq8, w_scale, N_total, Y, y_dtype, ldy, comm, ws, ws_bytes, e4m3,
-                                nsm, static_cast<cudaStream_t>(stream));
+                                swiglu, nsm, static_cast<cudaStream_t>(stream));
   const int world = comm ? comm->world : 1;
   if (N_total < 1 || N_total % world)
     return fail(RRS_ERR_INVALID_ARGUMENT, "N_total=%lld must be a positive multiple of world=%d", (long long)N_total, world);
@@ -376,20 +384,23 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
   const int esz = y_dtype == RRS_F32 ? 4 : 2;
   if (world == 1) {
-    if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy)) return s;
+    if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy, swiglu)) return s;
     rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N_total, K, group, out_scale, false, e4m3, Y,
-                    y_dtype, ldy, nullptr};
+                    y_dtype, ldy, nullptr, swiglu};
     cudaError_t e = rrs::launch_gemm(a, nsm, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
   }
   // column-parallel: local shard [T][n_local] -> all-gather [world][T][n_local] -> Y[T][ldy]
-  if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, n_local, K, group, w.y_shard, n_local)) return s;
-  if (ldy < N_total || !aligned16(Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "Y / ldy");
+  // with the fused SwiGLU each rank's shard holds whole (gate, up) pairs and yields n_local / 2 outputs
+  const int64_t n_out_local = swiglu ? n_local / 2 : n_local, n_out = swiglu ? N_total / 2 : N_total;
+  if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, n_local, K, group, w.y_shard, n_out_local, swiglu))
+    return s;
+  if (ldy < n_out || !aligned16(Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "Y / ldy");
   rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, n_local, K, group, out_scale, false, e4m3,
-                  w.y_shard, y_dtype, n_local, nullptr};
+                  w.y_shard, y_dtype, n_out_local, nullptr, swiglu};
   cudaError_t e = rrs::launch_gemm(a, nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "rrs_gemm kernel");
-  return gather_columns(w.y_shard, T, N_total, esz, Y, ldy, comm, w.y_gather, st);
+  return gather_columns(w.y_shard, T, n_out, esz, Y, ldy, comm, w.y_gather, st);
 }
 
 rrs_status rrs_allgather_columns(const void* Y_shard, int64_t T, int64_t N_total, int32_t y_dtype, void* Y,

@@ -108,6 +108,7 @@ struct GemmParams {
   int64_t ldy;
   int32_t* P_debug;
   int y_tma;  // bf16 Y written by TMA tensor stores (16-byte aligned base, ldy % 8 == 0)
+  int swiglu; // W rows interleaved (gate_i, up_i); Y[t][i] = bf16(silu(y_2i) * y_2i+1)
 };
 
 template <bool kPlain, bool kF32Out, bool kDebug, int kCta, bool kFp8>
@@ -514,6 +515,30 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
               ptx::bulk_commit_group();
               if (trace_epi) gtrace(8 * it + 4, 7);
             }
+          } else if (p.swiglu) {
+            // fused SwiGLU: this thread's column pairs (2i, 2i+1) are (gate_i, up_i), so
+            // h_i = silu(g) * u = g / (1 + e^-g) * u in f32, rounded once to bf16; 8 outputs per 16-byte store
+            __nv_bfloat16* hrow = reinterpret_cast<__nv_bfloat16*>(p.Y) + (int64_t)row * p.ldy;
+            auto swiglu1 = [](float2 v) { return v.x / (1.0f + expf(-v.x)) * v.y; };
+#pragma unroll
+            for (int c = 0; c < EPI_COLS; c += 16) {
+              uint32_t w[4];
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const float h0 = swiglu1(__fmul2_rn(acc2[c / 2 + 2 * h], beta2[c / 2 + 2 * h]));
+                const float h1 = swiglu1(__fmul2_rn(acc2[c / 2 + 2 * h + 1], beta2[c / 2 + 2 * h + 1]));
+                const __nv_bfloat162 bb = __floats2bfloat162_rn(h0, h1);
+                w[h] = *reinterpret_cast<const uint32_t*>(&bb);
+              }
+              const int i = (col0 + c) >> 1, nh = p.N >> 1;
+              if (i + 7 < nh) {
+                *reinterpret_cast<uint4*>(hrow + i) = make_uint4(w[0], w[1], w[2], w[3]);
+              } else {
+                const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(w);
+                for (int h = 0; h < 8; ++h)
+                  if (i + h < nh) hrow[i + h] = e[h];
+              }
+            }
           } else {
             __nv_bfloat16* yrow = reinterpret_cast<__nv_bfloat16*>(p.Y) + (int64_t)row * p.ldy;
 #pragma unroll
@@ -641,7 +666,9 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   CUtensorMap ty;
   memset(&ty, 0, sizeof(ty));
   p.y_tma = 0;
-  if (a.Y && a.y_dtype != 1 && !a.P_debug && a.ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0)
+  p.swiglu = a.swiglu ? 1 : 0;
+  if (a.swiglu && (a.y_dtype == 1 || a.plain || a.P_debug || a.N % 2)) return cudaErrorInvalidValue;
+  if (!a.swiglu && a.Y && a.y_dtype != 1 && !a.P_debug && a.ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0)
     p.y_tma = make_tmap_y(&ty, a.Y, a.T, a.N, a.ldy) ? 1 : 0;
   const int grid = std::min(p.num_tiles, nsm / kCta) * kCta;
   const bool f32 = a.y_dtype == 1;

@@ -62,6 +62,7 @@ struct GemmArgs {
   int y_dtype;            // 0 = bf16, 1 = f32
   int64_t ldy;
   int32_t* P_debug;       // optional [G][T][N] export of the int32 group partials (test only)
+  bool swiglu = false;    // bf16 Y[T][N/2] = silu(gate) * up of interleaved (gate_i, up_i) rows
 };
 cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st);
 

@@ -280,6 +280,58 @@ def test_rrs_linear_group_variants(T, N, K, group, i8):
     assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
 
 
+def test_swiglu_epilogue():
+    """RRS_GEMM_SWIGLU: with interleaved (gate, up) rows the bf16 output is, within 1 bf16 ulp,
+    bf16(silu(y_2i) * y_2i+1) of the very same GEMM's f32 output (the epilogue math is f32: one f32 product with
+    beta, e^-g and a division), and that f32 output meets the §5 bar against the oracle."""
+    T, F, K = 257, 260, 4096
+    X_bits, W_bits, perm, ref = _gemm_case(T, 2 * F, K, "mixed", seed=7)
+    Xq8 = _dev(encode_operand(ref["q"], False))
+    Wq8 = _dev(encode_operand(ref["qw"], False))
+    xs, sg, ws = (torch.from_numpy(ref[k]).to(DEV) for k in ("alpha", "s_group", "beta"))
+    Yf = torch.empty((T, 2 * F), dtype=torch.float32, device=DEV)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf, 1.0 / K)
+    H = torch.full((T, F + 4), float("nan"), dtype=torch.bfloat16, device=DEV)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, H[:, :F], 1.0 / K, swiglu=True)
+    torch.cuda.synchronize()
+    Y = Yf.cpu().numpy().astype(np.float64)
+    assert y_normalised_error(Yf.cpu().numpy(), ref) <= 1e-5
+    h_ref = o.swiglu(Y[:, 0::2], Y[:, 1::2])
+    Hn = H.float().cpu().numpy()
+    assert np.isnan(Hn[:, F:]).all()  # nothing written past N/2
+    assert bf16_ulp_error(Hn[:, :F], h_ref) <= 1.0
+
+
+def test_rrs_mlp_block():
+    """LLaMA MLP with RRS on the up/gate input (one prologue, one GEMM over 2F interleaved rows,
+    fused SwiGLU) and on the down_proj input (K = F = 7168 = 28 * 256, the 28*2^m rotation).  Stage by stage:
+    up/gate f32 output vs the oracle, h vs bf16(swiglu(that output)), down output vs the oracle run on h."""
+    T, D, F = 130, 1024, 7168
+    X_bits = make_activations("channel", T, D, 950, 951)
+    Xc_bits = make_activations("channel", 64, D, 950, 952)
+    Wg, Wu, Wd = make_weights(F, D, 953), make_weights(F, D, 954), make_weights(D, F, 955)
+    perm_in = _perm(Xc_bits)
+    Wug = np.stack([Wg, Wu], axis=1).reshape(2 * F, D)
+    # calibration of the down_proj reorder on the oracle's h of the calibration tokens
+    cal = oracle_layer(Xc_bits, Wug, perm_in, keep_partials=False)
+    h_cal = o.bf16_round(o.swiglu(cal["Y"][:, 0::2], cal["Y"][:, 1::2]))
+    perm_mid = o.calibrate_perm(h_cal).astype(np.int32)
+    mlp = rrs.RRSMLP(dev_bf16(Wg), dev_bf16(Wu), dev_bf16(Wd), torch.from_numpy(perm_in).to(DEV),
+                     torch.from_numpy(perm_mid).to(DEV))
+    X = dev_bf16(X_bits)
+    Y = mlp(X, out_dtype=torch.float32)
+    h = mlp.up_gate(X)
+    ug_f32 = rrs.RRSLinear(dev_bf16(Wug), torch.from_numpy(perm_in).to(DEV))(X, out_dtype=torch.float32)
+    torch.cuda.synchronize()
+    ref_ug = oracle_layer(X_bits, Wug, perm_in)
+    assert y_normalised_error(ug_f32.cpu().numpy(), ref_ug) <= 1e-5
+    Yug = ug_f32.cpu().numpy().astype(np.float64)
+    assert bf16_ulp_error(h.float().cpu().numpy(), o.swiglu(Yug[:, 0::2], Yug[:, 1::2])) <= 1.0
+    h_bits = h.view(torch.int16).cpu().numpy().view(np.uint16)
+    ref_down = oracle_layer(h_bits, Wd, perm_mid)
+    assert y_normalised_error(Y.cpu().numpy(), ref_down) <= 1e-5
+
+
 def test_rrs_linear_equals_prologue_plus_gemm_bitwise():
     X_bits, W_bits, perm, ref = _gemm_case(200, 512, 4096)
     X = dev_bf16(X_bits)

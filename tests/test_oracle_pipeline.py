@@ -302,3 +302,17 @@ def test_keep_partials_false_matches():
     a = o.rrs_linear(X, W, perm)
     b = o.rrs_linear(X, W, perm, keep_partials=False)
     assert np.allclose(a["Y"], b["Y"], rtol=1e-14, atol=0)
+
+
+def test_swiglu_pins():
+    """oracle.swiglu against what the definition fixes: silu(0) = 0, the odd-part identity
+    silu(x) - silu(-x) = x (x sigma(x) + x sigma(-x) = x), the logistic function from scipy, and the limits."""
+    from scipy.special import expit
+    rng = np.random.default_rng(7)
+    g = rng.normal(0, 4, 1000)
+    u = rng.normal(0, 1, 1000)
+    assert np.all(o.swiglu(np.zeros(5), np.arange(5.0)) == 0)
+    np.testing.assert_allclose(o.swiglu(g, 1.0) - o.swiglu(-g, 1.0), g, rtol=1e-13, atol=1e-13)
+    np.testing.assert_allclose(o.swiglu(g, u), g * expit(g) * u, rtol=1e-13, atol=1e-300)
+    assert o.swiglu(np.array([800.0]), np.array([2.0]))[0] == 1600.0
+    assert o.swiglu(np.array([-800.0]), np.array([2.0]))[0] == 0.0
