@@ -28,7 +28,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from rrs_synth import WORKLOADS, make_layer  # noqa: E402
+from rrs_synth import WORKLOADS, make_layer, make_weights  # noqa: E402
 
 METRIC = "RRS A4W4 linear TOPS"
 INT8_OVER_BF16 = 2.0  # nominal dense int8 : bf16 tensor ratio (4.5 : 2.25 PFLOP/s, B200_PROFILING.md)
@@ -247,6 +247,53 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
     return res
 
 
+def measure_mlp(args, dev):
+    """SURVEY §8 f1 on config C3 (LLaMA-3-8B MLP, 4096-token prefill, D = 4096, F = 14336), single GPU:
+    h = SwiGLU fused into ONE RRS GEMM over the interleaved gate/up rows (one prologue on X), then the
+    down_proj RRS layer on h.  Ops = 2 T D (2F) + 2 T F D."""
+    import torch
+
+    import paper_2409_20361_b200 as rrs
+
+    wu = WORKLOADS["c3_llama3_8b_up"]
+    T, D, F = wu.T, wu.K, wu.N
+    X_bits, _, Xc_bits = make_layer(wu, index=list(WORKLOADS).index("c3_llama3_8b_up"), N=8)
+
+    def dev_bf16(b):
+        return torch.from_numpy(np.ascontiguousarray(b).view(np.int16)).to(dev).view(torch.bfloat16)
+
+    X, Xc = dev_bf16(X_bits), dev_bf16(Xc_bits)
+    Wg, Wu_, Wd = (dev_bf16(make_weights(*shape, seed)) for shape, seed in
+                   (((F, D), 7101), ((F, D), 7102), ((D, F), 7103)))
+    perm_in = rrs.calibrate_perm(Xc)
+    up_gate = rrs.RRSLinear(rrs.interleave_gate_up(Wg, Wu_), perm_in, swiglu=True)
+    perm_mid = rrs.calibrate_perm(up_gate(Xc))  # offline reorder of the down_proj input (R5)
+    down = rrs.RRSLinear(Wd, perm_mid)
+    del Wg, Wu_, Wd
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    h = torch.empty((T, F), dtype=torch.bfloat16, device=dev)
+    Y = torch.empty((T, D), dtype=torch.bfloat16, device=dev)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.warmup + args.steps)]
+    for ev in evs:
+        flush.zero_()
+        ev[0].record(stream)
+        up_gate(X, Y=h, stream=stream)
+        ev[1].record(stream)
+        down(h, Y=Y, stream=stream)
+        ev[2].record(stream)
+    torch.cuda.synchronize()
+    evs = evs[args.warmup:]
+    ug = float(np.median([e[0].elapsed_time(e[1]) for e in evs]))
+    dn = float(np.median([e[1].elapsed_time(e[2]) for e in evs]))
+    step = float(np.median([e[0].elapsed_time(e[2]) for e in evs]))
+    ops = 2.0 * T * D * 2 * F + 2.0 * T * F * D
+    return {"ms_per_step": step, "tops": ops / (step * 1e-3) / 1e12, "tokens_per_s": T / (step * 1e-3),
+            "breakdown_ms": {"up_gate_swiglu (prologue + one GEMM over 2F rows)": ug,
+                             "down_proj (K = 14336 prologue + GEMM)": dn},
+            "note": "SURVEY 8 f1: LLaMA-3-8B MLP block, T=4096 D=4096 F=14336, bf16 h and Y, L2 flushed per step"}
+
+
 def run_gpu(args):
     import torch
     import torch.distributed as dist
@@ -268,6 +315,10 @@ def run_gpu(args):
                             cpu_base=(world == 1 and not args.no_cpu_baseline))
     extras = {}
     for wn in (args.also.split(",") if args.also else []):
+        if wn == "c3_llama3_8b_mlp":
+            if world == 1:
+                extras[wn] = measure_mlp(args, dev)
+            continue
         r = measure_workload(args, wn, dev, world, rank, comm, cpu_base=False)
         if r is not None:
             extras[wn] = {k: r[k] for k in ("ms_per_step", "tops", "tokens_per_s", "breakdown_ms", "gemm_tops",
@@ -287,6 +338,7 @@ def run_gpu(args):
         with open(prof) as fh:
             traffic = json.load(fh).get(args.workload, {}).get("gemm_dram_bytes_per_launch")
     w = WORKLOADS[args.workload]
+    pow2 = (w.K & (w.K - 1)) == 0  # K = 2^m: the single-launch fused prologue
     out = {
         "metric": METRIC,
         "value": head["tops"],
@@ -318,8 +370,9 @@ def run_gpu(args):
         "e2e": {"value": head["e2e_tops"], "unit": "TOPS", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"],
                 "api": "rrs_linear (pinned host X -> device -> host Y, copies inside the timed region)"},
-        "gpu_launches": 3 + (1 if world > 1 else 0),
-        "gpu_launches_note": "per step: fwht_colmax_kernel, smooth_quant_kernel, rrs_gemm_kernel"
+        "gpu_launches": (2 if pow2 else 3) + (1 if world > 1 else 0),
+        "gpu_launches_note": "per step: " + ("prologue_fused_kernel" if pow2 else "fwht_colmax_kernel, smooth_quant_kernel")
+                             + ", rrs_gemm_kernel"
                              + (", relayout_kernel (+ ncclAllGather)" if world > 1 else "")
                              + " (+ one cudaMemsetAsync of chan_max)",
         "clocks": head["clocks"],
@@ -418,7 +471,7 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["rrs", "reference"], default="rrs")
     ap.add_argument("--workload", default="c3_llama3_8b_up", choices=sorted(WORKLOADS))
-    ap.add_argument("--also", default="c3_llama3_8b_down,c2_llama2_7b_qo",
+    ap.add_argument("--also", default="c3_llama3_8b_down,c2_llama2_7b_qo,c3_llama3_8b_mlp,c4_decode_t64,c4_decode_t1",
                     help="comma-separated extra workloads summarised under 'also' (empty: none)")
     ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)

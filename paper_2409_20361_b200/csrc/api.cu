@@ -97,7 +97,10 @@ struct Workspace {
   int8_t* Xq8;
   void* y_shard;
   void* y_gather;
+  float* part;      // split-K partials f32 [kMaxSplits][T][N] (decode-sized T only)
 };
+constexpr int kMaxSplits = 8;
+constexpr int64_t kSplitMaxT = 128;  // the single-CTA (M = 128) GEMM regime
 
 size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t world, Workspace* w) {
   size_t off = 0;
@@ -115,6 +118,7 @@ size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t
   ws.Xq8 = static_cast<int8_t*>(take((size_t)T * K));
   ws.y_shard = nullptr;
   ws.y_gather = nullptr;
+  ws.part = (T > 0 && T <= kSplitMaxT) ? static_cast<float*>(take(sizeof(float) * kMaxSplits * (size_t)T * N)) : nullptr;
   if (world > 1) {
     const int64_t ns = N / world;
     ws.y_shard = take((size_t)T * ns * 4);
@@ -318,6 +322,33 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
 }
 
+// Decode-sized T (one M = 128 row block): the (T, N) tile grid covers only N/240 SMs, so the K range is split
+// over up to kMaxSplits CTAs per tile (whole groups each) and a fixed-order reduction sums the f32 partials.
+static int choose_splits(int64_t T, int64_t N, int64_t K, int32_t group, int nsm, const float* part) {
+  if (!part || T > kSplitMaxT || N % 4) return 1;
+  const int64_t tiles = (N + 239) / 240, KB = K / 128, G = K / group;
+  int best = 1;
+  for (int s = 2; s <= kMaxSplits; ++s)
+    if (KB % s == 0 && G % s == 0 && tiles * s <= nsm) best = s;
+  return best;
+}
+
+// The layer's GEMM, split-K when it pays (then Y is written by the reduction kernel).
+static cudaError_t layer_gemm(rrs::GemmArgs a, const Workspace& w, int nsm, cudaStream_t st) {
+  const int splits = a.swiglu ? 1 : choose_splits(a.T, a.N, a.K, a.group, nsm, w.part);
+  if (splits == 1) return rrs::launch_gemm(a, nsm, st);
+  void* Y = a.Y;
+  const int y_dtype = a.y_dtype;
+  const int64_t ldy = a.ldy;
+  a.splits = splits;
+  a.Y = w.part;
+  a.y_dtype = 1;
+  a.ldy = a.N;
+  cudaError_t e = rrs::launch_gemm(a, nsm, st);
+  if (e != cudaSuccess) return e;
+  return rrs::launch_reduce_splits(w.part, splits, a.T, a.N, Y, y_dtype, ldy, st);
+}
+
 // token-sharded data parallel.  The prologue runs as its two passes (the fused single-kernel
 // prologue has a grid barrier where the cross-rank reduction must go): rotate + local channel max, one
 // ncclAllReduce(MAX) of chan_max[K] (non-negative floats: max is exact and order-free), smooth + quantise.
@@ -347,7 +378,7 @@ static rrs_status linear_token_sharded(const void* X, int64_t T, int64_t K, int3
   if (e != cudaSuccess) return cuda_fail(e, "smooth_quant_kernel");
   rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N, K, group, 1.0f / (float)K, false, e4m3, Y,
                   y_dtype, ldy, nullptr, swiglu};
-  e = rrs::launch_gemm(a, nsm, st);
+  e = layer_gemm(a, w, nsm, st);
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
 }
 
@@ -387,7 +418,7 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
     if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy, swiglu)) return s;
     rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N_total, K, group, out_scale, false, e4m3, Y,
                     y_dtype, ldy, nullptr, swiglu};
-    cudaError_t e = rrs::launch_gemm(a, nsm, st);
+    cudaError_t e = layer_gemm(a, w, nsm, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
   }
   // column-parallel: local shard [T][n_local] -> all-gather [world][T][n_local] -> Y[T][ldy]

@@ -103,6 +103,9 @@ struct GemmParams {
   int T, N, K, G;   // G = K / group smoothing groups
   int KB, gk;       // K-blocks of 128, MMA K-steps (of 32) per group
   int num_m, num_n, num_tiles;
+  int num_mn;              // output tiles; num_tiles = num_mn * splits
+  int splits, kps, gps;    // split-K (decode-sized T): K-blocks and groups per split
+  int64_t split_stride;    // elements between the f32 partial outputs of consecutive splits
   float out_scale;
   void* Y;
   int64_t ldy;
@@ -175,9 +178,10 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x / kCta; tile < p.num_tiles; tile += gridDim.x / kCta) {
-        const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
+        const int mn = tile % p.num_mn, kb0 = (tile / p.num_mn) * p.kps;
+        const int m_blk = mn % p.num_m, n_blk = mn / p.num_m;
         const int row0 = m_blk * BM * kCta + (int)rank * BM, wrow0 = n_blk * BN + (int)rank * C::B_ROWS;
-        for (int kb = 0; kb < p.KB; ++kb) {
+        for (int kb = kb0; kb < kb0 + p.kps; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if constexpr (kCta == 1) {
             ptx::mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
@@ -235,11 +239,11 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     };
     if (kPlain || gk >= 4) {
       // whole K-blocks per group (the hot path): 4 MMAs back to back per K-block
-      const int gpb = kPlain ? p.KB : gk / 4;  // K-blocks per accumulation
+      const int gpb = kPlain ? p.kps : gk / 4;  // K-blocks per accumulation
       for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
         int kin = 0;  // K-blocks into the current accumulation
-        for (int kb = 0; kb < p.KB; ++kb, it += (kb == p.KB)) {
-          const int trow = gtrace_row(it, kb, p.KB);
+        for (int kb = 0; kb < p.kps; ++kb, it += (kb == p.kps)) {
+          const int trow = gtrace_row(it, kb, p.kps);
           const uint32_t b = acc_iter & 1;
           if (kin == 0) wait_tempty(b);
           gtrace(trow, 0);
@@ -267,7 +271,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       // groups of 32 or 64 codes: gk = 1 or 2 MMA K-steps, several groups per K-block
       int ks = 0;  // K-steps of the current group issued so far
       for (int tile = blockIdx.x / kCta; leader && lane == 0 && tile < p.num_tiles; tile += gridDim.x / kCta) {
-        for (int kb = 0; kb < p.KB; ++kb) {
+        for (int kb = 0; kb < p.kps; ++kb) {
           wait_full();
           const uint64_t a_desc = a_desc0 + (uint64_t)((stage * A_BYTES) >> 4);
           const uint64_t b_desc = b_desc0 + (uint64_t)((stage * B_BYTES) >> 4);
@@ -337,7 +341,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     // Completion: cp.async.wait_group 0 + the epilogue's named barrier.
     auto fetch_xs = [&](int tile, int buf) {
       if (et < BM) {
-        const int r = (tile % p.num_m) * BM * kCta + (int)rank * BM + et;
+        const int r = ((tile % p.num_mn) % p.num_m) * BM * kCta + (int)rank * BM + et;
         const bool ok = tile < p.num_tiles && p.x_scale && r < p.T;
         ptx::cp_async4(xs_sm + buf * BM + et, ok ? p.x_scale + r : p.x_scale, ok ? 4u : 0u);
       }
@@ -347,7 +351,8 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     ptx::cp_async_wait_all();
     asm volatile("bar.sync 1, %0;" ::"n"(NUM_EPI_WARPS * 32));
     for (int tile = blockIdx.x / kCta; tile < p.num_tiles; tile += tile_stride, ++it) {
-      const int m_blk = tile % p.num_m, n_blk = tile / p.num_m;
+      const int mn = tile % p.num_mn, split = tile / p.num_mn;
+      const int m_blk = mn % p.num_m, n_blk = mn / p.num_m;
       const int row = m_blk * BM * kCta + (int)rank * BM + row_in_tile;
       const int col0 = n_blk * BN + half * EPI_COLS;
       // rs = alpha_t * out_scale is folded into every group's scale (acc = sum_g fl(s_g * rs) * P_g), so the
@@ -365,7 +370,8 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
 #pragma unroll
       for (int c = 0; c < EPI_COLS / 2; ++c) acc2[c] = make_float2(0.0f, 0.0f);
       if (it < 2 && lane == 0 && ew == 0) gtrace(8 * it + 6, 7);
-      const int ngroups = kPlain ? 1 : p.G;
+      const int ngroups = kPlain ? 1 : p.gps;
+      const float* s_split = s_sm + split * p.gps;  // this split's groups
       for (int g = 0; g < ngroups; ++g) {
         const uint32_t b = acc_iter & 1;
         // RRS: a buffer lands every group, spin for the lowest wake-up latency; plain: once per tile, sleep
@@ -377,7 +383,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         const bool trace_me = lane == 0 && (ew == 0 || ew == NUM_EPI_WARPS - 1);
         const int trow = gtrace_row(it, g, p.G);
         if (trace_me) gtrace(trow, ew == 0 ? 3 : 5);
-        const float s = kPlain ? rs : s_sm[g] * rs;
+        const float s = kPlain ? rs : s_split[g] * rs;
         const float2 s2 = make_float2(s, s);
         const uint32_t tbase = tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS;
 #if defined(RRS_TRACE) && defined(RRS_GEXP) && RRS_GEXP == 1
@@ -472,7 +478,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       const float2* beta2 = reinterpret_cast<const float2*>(beta_sm + (it & 1) * BN + half * EPI_COLS);
       if (p.Y != nullptr && (row < p.T || (!kF32Out && !kDebug && p.y_tma))) {
         if constexpr (kF32Out || kDebug) {
-          float* yrow = reinterpret_cast<float*>(p.Y) + (int64_t)row * p.ldy;
+          float* yrow = reinterpret_cast<float*>(p.Y) + split * p.split_stride + (int64_t)row * p.ldy;
 #pragma unroll
           for (int c = 0; c < EPI_COLS; c += 4) {
             const int n = col0 + c;
@@ -657,7 +663,15 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.gk = a.group / 32;
   p.num_m = (int)((a.T + BM * kCta - 1) / (BM * kCta));
   p.num_n = (int)((a.N + BN - 1) / BN);
-  p.num_tiles = p.num_m * p.num_n;
+  p.num_mn = p.num_m * p.num_n;
+  p.splits = a.splits;
+  p.kps = p.KB / a.splits;
+  p.gps = p.G / a.splits;
+  p.split_stride = (int64_t)a.T * a.ldy;
+  p.num_tiles = p.num_mn * a.splits;
+  // a split owns whole K-blocks and whole groups; split partials are f32 (reduced by reduce_splits_kernel)
+  if (a.splits < 1 || p.KB % a.splits || p.G % a.splits || (a.splits > 1 && (a.plain || a.y_dtype != 1 || a.swiglu)))
+    return cudaErrorInvalidValue;
   p.out_scale = a.out_scale;
   p.Y = a.Y;
   p.ldy = a.ldy;
@@ -668,7 +682,11 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.y_tma = 0;
   p.swiglu = a.swiglu ? 1 : 0;
   if (a.swiglu && (a.y_dtype == 1 || a.plain || a.P_debug || a.N % 2)) return cudaErrorInvalidValue;
-  if (!a.swiglu && a.Y && a.y_dtype != 1 && !a.P_debug && a.ldy % 8 == 0 && (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0)
+#ifndef RRS_GEMM_Y_TMA
+#define RRS_GEMM_Y_TMA 1  // experiment knob (bench/micro): 0 = per-thread 16-byte row stores for bf16 Y
+#endif
+  if (RRS_GEMM_Y_TMA && !a.swiglu && a.Y && a.y_dtype != 1 && !a.P_debug && a.ldy % 8 == 0 &&
+      (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0)
     p.y_tma = make_tmap_y(&ty, a.Y, a.T, a.N, a.ldy) ? 1 : 0;
   const int grid = std::min(p.num_tiles, nsm / kCta) * kCta;
   const bool f32 = a.y_dtype == 1;
@@ -687,6 +705,41 @@ cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st) {
   // CTA pairs (M = 256) once there are enough tokens to fill them; single CTAs for decode-sized T
   if (a.fp8) return a.T > BM ? launch_cta<2, true>(a, nsm, st) : launch_cta<1, true>(a, nsm, st);
   return a.T > BM ? launch_cta<2, false>(a, nsm, st) : launch_cta<1, false>(a, nsm, st);
+}
+
+// Split-K (decode-sized T): Y[t][n] = sum over splits s = 0, 1, ... (fixed order, deterministic, R15) of the
+// f32 partials part[s][t][n] (each already acc * beta); f32 or bf16 (RNE) out.  4 columns per thread.
+__global__ void reduce_splits_kernel(const float* __restrict__ part, int splits, int64_t T, int64_t N,
+                                     void* __restrict__ Y, int y_bf16, int64_t ldy) {
+  const int64_t nq = N / 4, total = T * nq;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t t = i / nq, n = (i % nq) * 4;
+    float4 acc = reinterpret_cast<const float4*>(part + t * N + n)[0];
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = reinterpret_cast<const float4*>(part + (s * T + t) * N + n)[0];
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    if (y_bf16) {
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(acc.x, acc.y), hi = __floats2bfloat162_rn(acc.z, acc.w);
+      uint2 w;
+      w.x = *reinterpret_cast<const uint32_t*>(&lo);
+      w.y = *reinterpret_cast<const uint32_t*>(&hi);
+      *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(Y) + t * ldy + n) = w;
+    } else {
+      *reinterpret_cast<float4*>(reinterpret_cast<float*>(Y) + t * ldy + n) = acc;
+    }
+  }
+}
+
+cudaError_t launch_reduce_splits(const float* part, int splits, int64_t T, int64_t N, void* Y, int y_dtype,
+                                 int64_t ldy, cudaStream_t st) {
+  if (N % 4) return cudaErrorInvalidValue;
+  const int64_t total = T * (N / 4);
+  if (total == 0) return cudaSuccess;
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>((total + threads - 1) / threads, 148 * 8);
+  reduce_splits_kernel<<<blocks, threads, 0, st>>>(part, splits, T, N, Y, y_dtype == 1 ? 0 : 1, ldy);
+  return cudaGetLastError();
 }
 
 // Y[t][r*ns + j] = gather[r][t][j]  (all-gathered column shards -> row-major Y), 16-byte chunks

@@ -63,7 +63,11 @@ struct GemmArgs {
   int64_t ldy;
   int32_t* P_debug;       // optional [G][T][N] export of the int32 group partials (test only)
   bool swiglu = false;    // bf16 Y[T][N/2] = silu(gate) * up of interleaved (gate_i, up_i) rows
+  int splits = 1;         // split-K: >1 writes f32 partials [splits][T][ldy] to Y (then launch_reduce_splits)
 };
+// Y = sum of the split-K partials [splits][T][N] f32 (fixed order), f32 or bf16 out
+cudaError_t launch_reduce_splits(const float* part, int splits, int64_t T, int64_t N, void* Y, int y_dtype,
+                                 int64_t ldy, cudaStream_t st);
 cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st);
 
 cudaError_t launch_relayout_shards(const void* src, void* dst, int64_t T, int64_t n_shard, int world,

@@ -280,6 +280,26 @@ def test_rrs_linear_group_variants(T, N, K, group, i8):
     assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
 
 
+@pytest.mark.parametrize("T,N,K,out", [(1, 1024, 8192, "f32"), (17, 1024, 8192, "bf16"), (64, 488, 8192, "f32"),
+                                       (100, 520, 14336, "f32"), (128, 264, 4096, "bf16")])
+def test_decode_split_k(T, N, K, out):
+    """Decode-sized T (<= 128, configs[3]): rrs_linear splits K over up to 8 CTAs per output tile (whole groups
+    each) and sums the f32 partials in a fixed order -- same bar against the oracle, deterministic."""
+    X_bits, W_bits, perm, ref = _gemm_case(T, N, K, "mixed", seed=T)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV))
+    X = dev_bf16(X_bits)
+    if out == "f32":
+        Y = layer(X, out_dtype=torch.float32)
+        Y2 = layer(X, out_dtype=torch.float32)
+        torch.cuda.synchronize()
+        assert torch.equal(Y, Y2)
+        assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
+    else:
+        Y = layer(X, out_dtype=torch.bfloat16)
+        torch.cuda.synchronize()
+        assert bf16_ulp_error(Y.float().cpu().numpy(), ref["Y"], ref) <= 1.0
+
+
 def test_swiglu_epilogue():
     """RRS_GEMM_SWIGLU: with interleaved (gate, up) rows the bf16 output is, within 1 bf16 ulp,
     bf16(silu(y_2i) * y_2i+1) of the very same GEMM's f32 output (the epilogue math is f32: one f32 product with
