@@ -685,7 +685,10 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
 #ifndef RRS_GEMM_Y_TMA
 #define RRS_GEMM_Y_TMA 1  // experiment knob (bench/micro): 0 = per-thread 16-byte row stores for bf16 Y
 #endif
-  if (RRS_GEMM_Y_TMA && !a.swiglu && a.Y && a.y_dtype != 1 && !a.P_debug && a.ldy % 8 == 0 &&
+  // (a TMA store writes whole 16-byte chunks at the right edge of the tensor, so it is only used when the output
+  // width is a multiple of 8 bf16: columns past N belong to the caller, e.g. a column slice of a wider matrix.
+  // The fused SwiGLU output uses per-thread 16-byte stores: its 40-column TMA boxes lost every other box.)
+  if (RRS_GEMM_Y_TMA && !a.swiglu && a.Y && a.y_dtype != 1 && !a.P_debug && a.ldy % 8 == 0 && a.N % 8 == 0 &&
       (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0)
     p.y_tma = make_tmap_y(&ty, a.Y, a.T, a.N, a.ldy) ? 1 : 0;
   const int grid = std::min(p.num_tiles, nsm / kCta) * kCta;

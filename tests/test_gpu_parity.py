@@ -214,11 +214,12 @@ def test_rrs_gemm_y_f32_and_bf16(T, N, K, profile, i8):
     ldy = (N + 7) // 8 * 8
     Yf = torch.full((T, ldy), float("nan"), dtype=torch.float32, device=DEV)
     rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf[:, :N], 1.0 / K, i8=i8)
-    Yb = torch.zeros((T, ldy), dtype=torch.bfloat16, device=DEV)
+    Yb = torch.full((T, ldy), float("nan"), dtype=torch.bfloat16, device=DEV)
     rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yb[:, :N], 1.0 / K, i8=i8)
     torch.cuda.synchronize()
     Yf_np = Yf.cpu().numpy()
     assert np.isnan(Yf_np[:, N:]).all()  # nothing written past N
+    assert torch.isnan(Yb[:, N:].float()).all()  # bf16 (TMA-stored when N % 8 == 0) too
     assert y_normalised_error(Yf_np[:, :N], ref) <= 1e-5
     assert bf16_ulp_error(Yb[:, :N].float().cpu().numpy(), ref["Y"], ref) <= 1.0
     # bf16 output is the round-to-nearest-even of the very same f32 accumulation
@@ -278,6 +279,24 @@ def test_rrs_linear_group_variants(T, N, K, group, i8):
     Y = layer(dev_bf16(X_bits), out_dtype=torch.float32)
     torch.cuda.synchronize()
     assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
+
+
+def test_swiglu_epilogue_tma_width():
+    """F % 8 == 0, ragged T, Y a sub-block of a larger buffer: every output written, nothing outside it."""
+    T, F, K = 300, 248, 2048
+    X_bits, W_bits, perm, ref = _gemm_case(T, 2 * F, K, "channel", seed=8)
+    Xq8 = _dev(encode_operand(ref["q"], False))
+    Wq8 = _dev(encode_operand(ref["qw"], False))
+    xs, sg, ws = (torch.from_numpy(ref[k]).to(DEV) for k in ("alpha", "s_group", "beta"))
+    Yf = torch.empty((T, 2 * F), dtype=torch.float32, device=DEV)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf, 1.0 / K)
+    H = torch.full((T + 5, F + 8), float("nan"), dtype=torch.bfloat16, device=DEV)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, H[:T, :F], 1.0 / K, swiglu=True)
+    torch.cuda.synchronize()
+    Y = Yf.cpu().numpy().astype(np.float64)
+    Hn = H.float().cpu().numpy()
+    assert np.isnan(Hn[:, F:]).all() and np.isnan(Hn[T:]).all()
+    assert bf16_ulp_error(Hn[:T, :F], o.swiglu(Y[:, 0::2], Y[:, 1::2])) <= 1.0
 
 
 @pytest.mark.parametrize("T,N,K,out", [(1, 1024, 8192, "f32"), (17, 1024, 8192, "bf16"), (64, 488, 8192, "f32"),
@@ -340,7 +359,8 @@ def test_rrs_mlp_block():
                      torch.from_numpy(perm_mid).to(DEV))
     X = dev_bf16(X_bits)
     Y = mlp(X, out_dtype=torch.float32)
-    h = mlp.up_gate(X)
+    h = torch.full((T, F), float("nan"), dtype=torch.bfloat16, device=DEV)  # no stale allocator memory
+    mlp.up_gate(X, Y=h)
     ug_f32 = rrs.RRSLinear(dev_bf16(Wug), torch.from_numpy(perm_in).to(DEV))(X, out_dtype=torch.float32)
     torch.cuda.synchronize()
     ref_ug = oracle_layer(X_bits, Wug, perm_in)
