@@ -182,6 +182,12 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
     per_step = [e[0].elapsed_time(e[1]) for e in evs]
 
     # ---- breakdown (separate pass, events between the kernels): prologue / GEMM / all-gather / plain GEMM
+    # (+ the sub-channel baseline GEMM: its per-group scales are arbitrary positive numbers -- its speed does
+    # not depend on their values -- so this times the kernel, not a quantisation)
+    sub_ok = n_local % 8 == 0
+    G = K // 128
+    sub_xs = torch.rand((G, T), dtype=torch.float32, device=dev) + 0.5
+    sub_ws = torch.rand((G, n_local), dtype=torch.float32, device=dev) + 0.5
     bev = new_events(args.steps, 5)
     for i in range(args.warmup + args.steps):
         ev = bev[i - args.warmup] if i >= args.warmup else new_events(1, 5)[0]
@@ -199,11 +205,19 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         rrs.rrs_gemm(Xop, xs, None, layer.Wop, layer.w_scale, Y_shard, out_scale, plain=True, stream=stream)
         ev.append(torch.cuda.Event(enable_timing=True))
         ev[5].record(stream)
+        if sub_ok:  # sub-channel A4W4 GEMM (P:322's second baseline) on the same codes
+            flush.zero_()
+            ev.append(torch.cuda.Event(enable_timing=True))
+            ev.append(torch.cuda.Event(enable_timing=True))
+            ev[6].record(stream)
+            rrs.rrs_gemm(Xop, sub_xs, None, layer.Wop, sub_ws, Y_shard, out_scale, subchannel=True, stream=stream)
+            ev[7].record(stream)
     torch.cuda.synchronize()
     prologue = [e[0].elapsed_time(e[1]) for e in bev]
     gemm = [e[1].elapsed_time(e[2]) for e in bev]
     gather = [e[2].elapsed_time(e[3]) for e in bev]
     plain = [e[4].elapsed_time(e[5]) for e in bev]
+    subch = [e[6].elapsed_time(e[7]) for e in bev] if sub_ok else [0.0]
 
     # ---- end to end through the public API with host buffers: pinned H2D of X, rrs_linear, D2H of Y
     X_host = X.cpu().pin_memory()
@@ -225,7 +239,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         return max_over_ranks(vals, dev, world)
 
     ms_step, ms_pro, ms_gemm, ms_gather = mx(per_step), mx(prologue), mx(gemm), mx(gather)
-    ms_plain, ms_e2e = mx(plain), mx(e2e)
+    ms_plain, ms_e2e, ms_sub = mx(plain), mx(e2e), mx(subch)
     ck = clocks.summary()
     if world > 1:
         dist.barrier()
@@ -237,7 +251,8 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         "workload": wname, "T": T, "K": K, "N": N, "ms_per_step": ms_step,
         "tops": ops / (ms_step * 1e-3) / 1e12, "tokens_per_s": T / (ms_step * 1e-3),
         "breakdown_ms": {"prologue": ms_pro, "rrs_gemm": ms_gemm, "allgather": ms_gather,
-                         "plain_gemm": ms_plain, "prepare_weights_offline": prep_ms},
+                         "plain_gemm": ms_plain, "subchannel_gemm": ms_sub if sub_ok else None,
+                         "prepare_weights_offline": prep_ms},
         "gemm_tops": gemm_tops, "rrs_overhead_vs_plain_gemm": ms_gemm / ms_plain - 1.0,
         "e2e_tops": ops / (ms_e2e * 1e-3) / 1e12, "h2d": T * K * 2, "d2h": T * N * esz,
         "clocks": ck, "wall_s_timed_region": wall,

@@ -63,6 +63,7 @@ typedef enum { RRS_BF16 = 0, RRS_F32 = 1 } rrs_dtype;
 #define RRS_GEMM_PLAIN 0x1u   /* rrs_gemm: per-channel A4W4 baseline: one sum over all K, no s_g */
 #define RRS_OPERAND_I8 0x2u   /* GEMM operands are int8 codes (tcgen05 .kind::i8) instead of E4M3 bytes */
 #define RRS_GEMM_SWIGLU 0x8u  /* rrs_gemm / rrs_linear: fused SwiGLU epilogue, see rrs_gemm */
+#define RRS_GEMM_SUBCHANNEL 0x10u /* rrs_gemm: sub-channel A4W4 baseline, see rrs_gemm */
 #define RRS_TOKEN_SHARDED 0x4u /* rrs_linear with comm: token-sharded data parallel, see below */
 
 typedef struct rrs_comm_s* rrs_comm_t;
@@ -121,6 +122,10 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
  * out_scale = 1/K after rotation (R1).  flags & RRS_GEMM_PLAIN: per-channel A4W4 baseline
  * Y = out_scale * alpha_t * beta_n * sum_{all j'} q qw (s_group ignored, may be NULL).
  * flags & RRS_OPERAND_I8: operands are int8 codes, else E4M3 bytes (see the conventions above).
+ * flags & RRS_GEMM_SUBCHANNEL (the second efficiency baseline of P:322): x_scale is
+ *   alpha f32 [G][T] and w_scale beta f32 [G][N] (per token / per output row AND per group of `group` codes,
+ *   sub-channel RTN), s_group is ignored: Y = out_scale * sum_g alpha_gt * beta_gn * P_g.  E4M3 operands only,
+ *   N % 8 == 0, scales 16-byte aligned.
  * flags & RRS_GEMM_SWIGLU (LLaMA MLP; P:138 places RRS on the up/gate and down inputs): the N
  *   weight rows are interleaved gate/up pairs (row 2i = gate_i, row 2i+1 = up_i, N even) and Y receives
  *   bf16 [T][N/2] with Y[t][i] = bf16_rne(silu(y_2i) * y_2i+1), y = the f32 layer output above and

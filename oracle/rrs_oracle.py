@@ -306,6 +306,30 @@ def bf16_round(y: np.ndarray) -> np.ndarray:
 # ----------------------------------------------------------------------------------------
 
 
+def subchannel_quant(A: np.ndarray, L: int):
+    """Sub-channel symmetric INT4 RTN (the second efficiency baseline of P:322): every row is
+    quantised group by group, each group of L consecutive columns with its own scale, by the same per-row rule as
+    quantize_rows (R9-R12).  Returns (q int8 [R][K], alpha f32 [G][R])."""
+    A = np.asarray(A, dtype=F32)
+    R, K = A.shape
+    if K % L:
+        raise ValueError("K % group != 0")
+    q = np.zeros((R, K), dtype=np.int8)
+    alpha = np.zeros((K // L, R), dtype=F32)
+    for g in range(K // L):
+        q[:, g * L:(g + 1) * L], alpha[g] = quantize_rows(A[:, g * L:(g + 1) * L])
+    return q, alpha
+
+
+def subchannel_gemm(q: np.ndarray, qw: np.ndarray, alpha: np.ndarray, beta: np.ndarray, L: int,
+                    out_scale: float = 1.0) -> np.ndarray:
+    """Y[t][n] = out_scale * sum_g alpha[g][t] * beta[g][n] * P_g[t][n], in float64 (P:322's sub-channel A4W4)."""
+    P = group_partials(q, qw, L).astype(np.float64)
+    a = np.asarray(alpha, dtype=np.float64)
+    b = np.asarray(beta, dtype=np.float64)
+    return out_scale * np.einsum("gt,gn,gtn->tn", a, b, P)
+
+
 def swiglu(g: np.ndarray, u: np.ndarray) -> np.ndarray:
     """LLaMA MLP gate (the paper applies RRS to the up/gate and down_proj inputs of this block,
     P:138): h = silu(g) * u = g / (1 + exp(-g)) * u, in float64 (the definition, written out)."""

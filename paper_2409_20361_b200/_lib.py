@@ -21,6 +21,7 @@ RRS_GEMM_PLAIN = 0x1
 RRS_OPERAND_I8 = 0x2
 RRS_TOKEN_SHARDED = 0x4
 RRS_GEMM_SWIGLU = 0x8
+RRS_GEMM_SUBCHANNEL = 0x10
 
 _c_i64, _c_i32, _c_u32, _c_p, _c_sz, _c_f = (ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p,
                                              ctypes.c_size_t, ctypes.c_float)
@@ -153,10 +154,12 @@ def rrs_rotate_smooth_quant(X, perm, Xq, Xop, x_scale, s_group, chan_max=None, w
 
 
 def rrs_gemm(Xop, x_scale, s_group, Wop, w_scale, Y, out_scale: float, plain: bool = False, group: int = 128,
-             i8: bool = False, swiglu: bool = False, stream=None) -> None:
+             i8: bool = False, swiglu: bool = False, subchannel: bool = False, stream=None) -> None:
+    """subchannel: x_scale f32 [G][T], w_scale f32 [G][N] (the sub-channel A4W4 baseline), s_group unused."""
     T, K = Xop.shape
     N = Wop.shape[0]
-    flags = (RRS_GEMM_PLAIN if plain else 0) | _op_flags(i8) | (RRS_GEMM_SWIGLU if swiglu else 0)
+    flags = (RRS_GEMM_PLAIN if plain else 0) | _op_flags(i8) | (RRS_GEMM_SWIGLU if swiglu else 0) \
+        | (RRS_GEMM_SUBCHANNEL if subchannel else 0)
     _check("rrs_gemm",
            lib().rrs_gemm(_ptr(Xop), _ptr(x_scale), _ptr(s_group), _ptr(Wop), _ptr(w_scale), T, N, K, group,
                           float(out_scale), flags, _ptr(Y, True), _y_code(Y), Y.stride(0), _stream(stream)))

@@ -311,13 +311,18 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
   const bool swiglu = (flags & RRS_GEMM_SWIGLU) != 0;
   if (rrs_status s = gemm_checks(Xq8, x_scale, Wq8, w_scale, T, N, K, group, Y, ldy, swiglu)) return s;
   const bool plain = (flags & RRS_GEMM_PLAIN) != 0;
+  const bool sub = (flags & RRS_GEMM_SUBCHANNEL) != 0;
+  if (sub && (plain || swiglu || (flags & RRS_OPERAND_I8) || N % 8 || !aligned16(w_scale)))
+    return fail(RRS_ERR_INVALID_ARGUMENT,
+                "RRS_GEMM_SUBCHANNEL: E4M3 operands, N %% 8 == 0, 16-byte aligned scales, no PLAIN / SWIGLU");
   if (swiglu && (plain || y_dtype != RRS_BF16))
     return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_GEMM_SWIGLU: bf16 output of the RRS (not plain) GEMM only");
-  if (!plain && !s_group) return fail(RRS_ERR_INVALID_ARGUMENT, "s_group is NULL");
+  if (!plain && !sub && !s_group) return fail(RRS_ERR_INVALID_ARGUMENT, "s_group is NULL");
   if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
   if (T == 0) return RRS_OK;
   rrs::GemmArgs a{Xq8, x_scale, s_group, Wq8, w_scale, T, N, K, group, out_scale, plain,
                   (flags & RRS_OPERAND_I8) == 0, Y, y_dtype, ldy, nullptr, swiglu};
+  a.subchannel = sub;
   cudaError_t e = rrs::launch_gemm(a, nsm, static_cast<cudaStream_t>(stream));
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
 }

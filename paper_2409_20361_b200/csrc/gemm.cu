@@ -111,10 +111,14 @@ struct GemmParams {
   int64_t ldy;
   int32_t* P_debug;
   int y_tma;  // bf16 Y written by TMA tensor stores (16-byte aligned base, ldy % 8 == 0)
+  const int8_t* w_codes;  // Wq8 (for the decode-path L2 prefetch)
+  int w_l2_prefetch;
   int swiglu; // W rows interleaved (gate_i, up_i); Y[t][i] = bf16(silu(y_2i) * y_2i+1)
 };
 
-template <bool kPlain, bool kF32Out, bool kDebug, int kCta, bool kFp8>
+// kSub: the sub-channel A4W4 baseline of P:322 -- x_scale is alpha[G][T] and w_scale beta[G][N]
+// (per token / per output row AND per group), Y = out_scale * sum_g alpha_gt * beta_gn * P_g; s_group unused.
+template <bool kPlain, bool kF32Out, bool kDebug, int kCta, bool kFp8, bool kSub = false>
 __global__ void __launch_bounds__(gemm::THREADS, 1)
 rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_w,
                 const __grid_constant__ CUtensorMap tmap_y, GemmParams p) {
@@ -163,6 +167,20 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   }
   if (threadIdx.x < 8) bias_sm[threadIdx.x] = 0x4B400000u;
   if constexpr (kCta == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrive / TMA
+  if constexpr (kCta == 1) {
+    // decode-sized T: the GEMM streams W (an offline input) from HBM and little else.  Under programmatic
+    // dependent launch this grid starts while the prologue still runs (it occupies few SMs at this T), so
+    // the producer warp pulls this CTA's whole W slice into L2 before waiting for the prologue's results.
+    if (p.w_l2_prefetch && warp == 2) {
+      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        const int mn = tile % p.num_mn, kb0 = (tile / p.num_mn) * p.kps;
+        const int n0 = (mn / p.num_m) * BN;
+        const uint32_t bytes = (uint32_t)p.kps * BK;
+        for (int r = lane; r < BN && n0 + r < p.N; r += 32)
+          ptx::prefetch_l2_bulk(p.w_codes + (int64_t)(n0 + r) * p.K + (int64_t)kb0 * BK, bytes);
+      }
+    }
+  }
   ptx::pdl_wait();  // Xq8 / x_scale / s_group come from the prologue kernels (programmatic dependent launch)
   if (!kPlain && p.s_group) {
     for (int g = threadIdx.x; g < p.G; g += blockDim.x) s_sm[g] = p.s_group[g];
@@ -342,7 +360,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     auto fetch_xs = [&](int tile, int buf) {
       if (et < BM) {
         const int r = ((tile % p.num_mn) % p.num_m) * BM * kCta + (int)rank * BM + et;
-        const bool ok = tile < p.num_tiles && p.x_scale && r < p.T;
+        const bool ok = !kSub && tile < p.num_tiles && p.x_scale && r < p.T;
         ptx::cp_async4(xs_sm + buf * BM + et, ok ? p.x_scale + r : p.x_scale, ok ? 4u : 0u);
       }
     };
@@ -357,11 +375,15 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       const int col0 = n_blk * BN + half * EPI_COLS;
       // rs = alpha_t * out_scale is folded into every group's scale (acc = sum_g fl(s_g * rs) * P_g), so the
       // epilogue is a single multiply by beta_n
-      const float rs = xs_sm[(it & 1) * BM + row_in_tile] * p.out_scale;
+      const float rs = kSub ? p.out_scale : xs_sm[(it & 1) * BM + row_in_tile] * p.out_scale;
       if (et < BN) {
         const int n = n_blk * BN + et;
-        const bool ok = p.w_scale && n < p.N;
-        ptx::cp_async4(beta_sm + (it & 1) * BN + et, ok ? p.w_scale + n : p.w_scale, ok ? 4u : 0u);
+        if constexpr (kSub) {
+          beta_sm[(it & 1) * BN + et] = 1.0f;  // beta_gn already applied per group
+        } else {
+          const bool ok = p.w_scale && n < p.N;
+          ptx::cp_async4(beta_sm + (it & 1) * BN + et, ok ? p.w_scale + n : p.w_scale, ok ? 4u : 0u);
+        }
       }
       fetch_xs(tile + tile_stride, (it + 1) & 1);
       ptx::cp_async_commit();
@@ -394,7 +416,35 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
           acc2[g % (EPI_COLS / 2)].x += s;
         } else
 #endif
-        if constexpr (kFp8 && !kDebug) {
+        if constexpr (kSub) {
+          // sub-channel: every element has its own scale alpha_gt * beta_gn (beta read through L1, the 32 lanes
+          // of a warp share its 80 columns), applied per group before the FP32 accumulation
+          const float a = row < p.T ? __ldg(p.x_scale + (int64_t)(split * p.gps + g) * p.T + row) * rs : 0.0f;
+          const float* bg = p.w_scale + (int64_t)(split * p.gps + g) * p.N + col0;
+#pragma unroll
+          for (int cc = 0; cc < EPI_COLS / 16; ++cc) {
+            uint32_t r[16];
+            RRS_TMEM_LD16(tbase + cc * 16, r);
+            RRS_TMEM_WAIT_LD16(r);
+            if (cc == EPI_COLS / 16 - 1) {  // every column of this buffer is in registers: release it
+              ptx::tc_fence_before();
+              __syncwarp();
+              if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int n = col0 + cc * 16 + 4 * q;
+              const float4 bv = n < p.N ? __ldg(reinterpret_cast<const float4*>(bg + cc * 16 + 4 * q))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+              const float2 s01 = __fmul2_rn(make_float2(a, a), make_float2(bv.x, bv.y));
+              const float2 s23 = __fmul2_rn(make_float2(a, a), make_float2(bv.z, bv.w));
+              acc2[cc * 8 + 2 * q] = __ffma2_rn(s01, make_float2(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1])),
+                                                acc2[cc * 8 + 2 * q]);
+              acc2[cc * 8 + 2 * q + 1] = __ffma2_rn(
+                  s23, make_float2(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])), acc2[cc * 8 + 2 * q + 1]);
+            }
+          }
+        } else if constexpr (kFp8 && !kDebug) {
           // software-pipelined: chunk c+1 is in flight while chunk c is accumulated; the buffer is released
           // as soon as the last chunk has landed in registers
           constexpr int NCH = EPI_COLS / 16;
@@ -620,11 +670,11 @@ static bool make_tmap_y(CUtensorMap* m, void* base, int64_t T, int64_t N, int64_
   return r == CUDA_SUCCESS;
 }
 
-template <bool kPlain, bool kF32, bool kDebug, int kCta, bool kFp8>
+template <bool kPlain, bool kF32, bool kDebug, int kCta, bool kFp8, bool kSub = false>
 static cudaError_t launch_variant(const CUtensorMap& tx, const CUtensorMap& tw, const CUtensorMap& ty,
                                   const GemmParams& p, int grid,
                                   cudaStream_t st) {
-  auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug, kCta, kFp8>;
+  auto kern = rrs_gemm_kernel<kPlain, kF32, kDebug, kCta, kFp8, kSub>;
   constexpr int smem = gemm::Cfg<kCta>::SMEM_BYTES;
   cudaError_t e = prepare_kernel(kern, smem, gemm::THREADS);
   if (e != cudaSuccess) return e;
@@ -663,6 +713,8 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.gk = a.group / 32;
   p.num_m = (int)((a.T + BM * kCta - 1) / (BM * kCta));
   p.num_n = (int)((a.N + BN - 1) / BN);
+  p.w_codes = a.Wq8;
+  p.w_l2_prefetch = (kCta == 1 && !a.P_debug) ? 1 : 0;
   p.num_mn = p.num_m * p.num_n;
   p.splits = a.splits;
   p.kps = p.KB / a.splits;
@@ -694,6 +746,12 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   const int grid = std::min(p.num_tiles, nsm / kCta) * kCta;
   const bool f32 = a.y_dtype == 1;
   if (a.P_debug) return launch_variant<false, true, true, kCta, kFp8>(tx, tw, ty, p, grid, st);
+  if (a.subchannel) {
+    if constexpr (kFp8)
+      return f32 ? launch_variant<false, true, false, kCta, true, true>(tx, tw, ty, p, grid, st)
+                 : launch_variant<false, false, false, kCta, true, true>(tx, tw, ty, p, grid, st);
+    return cudaErrorInvalidValue;  // the baseline is built for the FP8 carrier only
+  }
   if (a.plain)
     return f32 ? launch_variant<true, true, false, kCta, kFp8>(tx, tw, ty, p, grid, st)
                : launch_variant<true, false, false, kCta, kFp8>(tx, tw, ty, p, grid, st);

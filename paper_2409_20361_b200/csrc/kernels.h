@@ -64,6 +64,7 @@ struct GemmArgs {
   int32_t* P_debug;       // optional [G][T][N] export of the int32 group partials (test only)
   bool swiglu = false;    // bf16 Y[T][N/2] = silu(gate) * up of interleaved (gate_i, up_i) rows
   int splits = 1;         // split-K: >1 writes f32 partials [splits][T][ldy] to Y (then launch_reduce_splits)
+  bool subchannel = false; // SURVEY §8 f4 baseline: x_scale alpha[G][T], w_scale beta[G][N], no s_group
 };
 // Y = sum of the split-K partials [splits][T][N] f32 (fixed order), f32 or bf16 out
 cudaError_t launch_reduce_splits(const float* part, int splits, int64_t T, int64_t N, void* Y, int y_dtype,

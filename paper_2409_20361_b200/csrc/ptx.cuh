@@ -96,6 +96,11 @@ RRS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
 }
 
 // ------------------------------------------------------------------ TMA
+// bulk prefetch of [gaddr, gaddr + bytes) into L2 (16-byte aligned, bytes % 16 == 0); no completion tracking
+RRS_DEV void prefetch_l2_bulk(const void* gaddr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gaddr)), "r"(bytes)
+               : "memory");
+}
 RRS_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }

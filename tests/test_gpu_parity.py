@@ -319,6 +319,36 @@ def test_decode_split_k(T, N, K, out):
         assert bf16_ulp_error(Y.float().cpu().numpy(), ref["Y"], ref) <= 1.0
 
 
+@pytest.mark.parametrize("T,N,K,group,out", [(300, 520, 2048, 128, "f32"), (129, 488, 4096, 256, "bf16"),
+                                             (64, 264, 1024, 64, "f32")])
+def test_subchannel_gemm_baseline(T, N, K, group, out):
+    """RRS_GEMM_SUBCHANNEL (SURVEY §8 f4, P:322's second efficiency baseline): per (token, group) and per
+    (row, group) RTN scales; Y within the §5 bar of the oracle's sum_g alpha_gt beta_gn P_g (f64)."""
+    X = bf16_bits_to_f64(make_activations("channel", T, K, 960, 961)).astype(np.float32)
+    W = bf16_bits_to_f64(make_weights(N, K, 962)).astype(np.float32)
+    q, a = o.subchannel_quant(X, group)
+    qw, b = o.subchannel_quant(W, group)
+    ref = o.subchannel_gemm(q, qw, a, b, group)
+    P = o.group_partials(q, qw, group).astype(np.float64)
+    den = np.einsum("gt,gn,gtn->tn", a.astype(np.float64), b.astype(np.float64), np.abs(P))
+    Xq8, Wq8 = _dev(encode_operand(q, False)), _dev(encode_operand(qw, False))
+    ta, tb = _dev(a), _dev(b)
+    if out == "f32":
+        Y = torch.full((T, N), float("nan"), dtype=torch.float32, device=DEV)
+        rrs.rrs_gemm(Xq8, ta, None, Wq8, tb, Y, 1.0, group=group, subchannel=True)
+        torch.cuda.synchronize()
+        err = np.abs(Y.cpu().numpy().astype(np.float64) - ref)
+        assert np.all(err <= 1e-5 * den + (den == 0) * 0.0)
+    else:
+        Y = torch.full((T, N), float("nan"), dtype=torch.bfloat16, device=DEV)
+        rrs.rrs_gemm(Xq8, ta, None, Wq8, tb, Y, 1.0, group=group, subchannel=True)
+        torch.cuda.synchronize()
+        ref_b = o.bf16_round(ref)
+        _, e = np.frexp(np.where(ref_b == 0, 1.0, ref_b))
+        ulp = np.ldexp(1.0, e - 8)
+        assert np.all(np.abs(Y.float().cpu().numpy().astype(np.float64) - ref_b) <= ulp + 1e-5 * den)
+
+
 def test_swiglu_epilogue():
     """RRS_GEMM_SWIGLU: with interleaved (gate, up) rows the bf16 output is, within 1 bf16 ulp,
     bf16(silu(y_2i) * y_2i+1) of the very same GEMM's f32 output (the epilogue math is f32: one f32 product with

@@ -316,3 +316,32 @@ def test_swiglu_pins():
     np.testing.assert_allclose(o.swiglu(g, u), g * expit(g) * u, rtol=1e-13, atol=1e-300)
     assert o.swiglu(np.array([800.0]), np.array([2.0]))[0] == 1600.0
     assert o.swiglu(np.array([-800.0]), np.array([2.0]))[0] == 0.0
+
+
+def test_subchannel_quant_and_gemm_pins():
+    """oracle.subchannel_* (SURVEY §8 f4): brute force on a tiny shape (per-element definition of the group
+    scale and code, triple-loop GEMM), and L = K reduces to the per-token / per-channel form."""
+    rng = np.random.default_rng(3)
+    T, N, K, L = 3, 4, 64, 32
+    X = rng.normal(0, 1, (T, K)).astype(np.float32)
+    W = rng.normal(0, 0.02, (N, K)).astype(np.float32)
+    X[1, 5] = 40.0  # one outlier: only its own group's scale may change
+    q, a = o.subchannel_quant(X, L)
+    qw, b = o.subchannel_quant(W, L)
+    for t in range(T):
+        for g in range(K // L):
+            m = np.float32(np.max(np.abs(X[t, g * L:(g + 1) * L])))
+            assert a[g, t] == np.float32(m / np.float32(7))
+            r = np.float32(np.float32(7) / m)
+            for j in range(g * L, (g + 1) * L):
+                assert q[t, j] == np.clip(np.rint(np.float32(X[t, j] * r)), -8, 7)
+    assert a[0, 1] > 4 * a[1, 1]  # the outlier group's scale, not the other group's
+    Y = o.subchannel_gemm(q, qw, a, b, L, out_scale=0.5)
+    for t in range(T):
+        for n in range(N):
+            ref = sum(float(a[g, t]) * float(b[g, n]) * sum(int(q[t, j]) * int(qw[n, j]) for j in range(g * L, (g + 1) * L))
+                      for g in range(K // L))
+            assert np.isclose(Y[t, n], 0.5 * ref, rtol=1e-12, atol=0)
+    q1, a1 = o.subchannel_quant(X, K)
+    qr, ar = o.quantize_rows(X)
+    assert np.array_equal(q1, qr) and np.array_equal(a1[0], ar)
