@@ -28,6 +28,7 @@
 // The MMA of group g+1 overlaps the promotion of group g (two TMEM buffers).  In plain mode (the
 // per-channel A4W4 baseline of P:322) the MMA accumulates all K into one buffer per tile instead.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -90,7 +91,7 @@ struct Cfg {
   static constexpr int EPI_TILE_BYTES = 32 * EPI_COLS * 2;  // one promotion warp's bf16 Y sub-tile (TMA store)
   static constexpr int SMEM_BYTES = 1024 /*align slack*/ + STAGES * STAGE_BYTES + NUM_EPI_WARPS * EPI_TILE_BYTES +
                                     1024 /*barriers*/ +
-                                    MAX_G * 4 + 2 * BN * 4 + 2 * BM * 4 + 64;
+                                    MAX_G * 4 + 2 * BN * 4 + 2 * BM * 4 + 64 + 3 * BN * 4;
   static_assert(B_ROWS % 8 == 0 && (STAGES * A_BYTES) % 1024 == 0 && B_BYTES % 1024 == 0, "swizzle atoms");
   static_assert(SMEM_BYTES <= 227 * 1024, "shared memory");
 };
@@ -141,6 +142,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   float* beta_sm = s_sm + MAX_G;     // [2][BN]   beta of the current tile (double-buffered by tile parity)
   float* xs_sm = beta_sm + 2 * BN;   // [2][BM]   alpha_t of the current / next tile's rows
   uint32_t* bias_sm = reinterpret_cast<uint32_t*>(xs_sm + 2 * BM);  // [8] = 0x4B400000
+  float* bsub_sm = reinterpret_cast<float*>(bias_sm + 16);            // [3][BN] sub-channel beta_g ring
 
   const uint32_t warp = ptx::warp_idx();
   const int lane = threadIdx.x & 31;
@@ -394,6 +396,26 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       if (it < 2 && lane == 0 && ew == 0) gtrace(8 * it + 6, 7);
       const int ngroups = kPlain ? 1 : p.gps;
       const float* s_split = s_sm + split * p.gps;  // this split's groups
+      // sub-channel: beta_g of this tile's columns staged in a 3-slot shared ring by cp.async two groups
+      // ahead (one named barrier per group), alpha_g of this thread's row prefetched one group ahead
+      auto fetch_bsub = [&](int g) {
+        if (g < ngroups && et < BN) {
+          const int n = n_blk * BN + et;
+          const bool ok = n < p.N;
+          const float* src = p.w_scale + (int64_t)(split * p.gps + g) * p.N + (ok ? n : 0);
+          ptx::cp_async4(bsub_sm + (g % 3) * BN + et, src, ok ? 4u : 0u);
+        }
+        ptx::cp_async_commit();  // possibly empty: one commit group per call keeps the wait counts uniform
+      };
+      auto load_alpha = [&](int g) {
+        return (g < ngroups && row < p.T) ? __ldg(p.x_scale + (int64_t)(split * p.gps + g) * p.T + row) : 0.0f;
+      };
+      float alpha_next = 0.0f;
+      if constexpr (kSub) {
+        fetch_bsub(0);
+        fetch_bsub(1);
+        alpha_next = load_alpha(0);
+      }
       for (int g = 0; g < ngroups; ++g) {
         const uint32_t b = acc_iter & 1;
         // RRS: a buffer lands every group, spin for the lowest wake-up latency; plain: once per tile, sleep
@@ -419,8 +441,12 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         if constexpr (kSub) {
           // sub-channel: every element has its own scale alpha_gt * beta_gn (beta read through L1, the 32 lanes
           // of a warp share its 80 columns), applied per group before the FP32 accumulation
-          const float a = row < p.T ? __ldg(p.x_scale + (int64_t)(split * p.gps + g) * p.T + row) * rs : 0.0f;
-          const float* bg = p.w_scale + (int64_t)(split * p.gps + g) * p.N + col0;
+          const float a = alpha_next * rs;
+          alpha_next = load_alpha(g + 1);
+          ptx::cp_async_wait_1();  // this thread's copies of group g have landed (g + 1 may be in flight)
+          asm volatile("bar.sync 2, %0;" ::"n"(NUM_EPI_WARPS * 32));  // ... and every thread's
+          const float4* bg4 = reinterpret_cast<const float4*>(bsub_sm + (g % 3) * BN + half * EPI_COLS);
+          fetch_bsub(g + 2);  // into the slot read in iteration g - 1, which every warp has left
 #pragma unroll
           for (int cc = 0; cc < EPI_COLS / 16; ++cc) {
             uint32_t r[16];
@@ -433,9 +459,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              const int n = col0 + cc * 16 + 4 * q;
-              const float4 bv = n < p.N ? __ldg(reinterpret_cast<const float4*>(bg + cc * 16 + 4 * q))
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+              const float4 bv = bg4[cc * 4 + q];
               const float2 s01 = __fmul2_rn(make_float2(a, a), make_float2(bv.x, bv.y));
               const float2 s23 = __fmul2_rn(make_float2(a, a), make_float2(bv.z, bv.w));
               acc2[cc * 8 + 2 * q] = __ffma2_rn(s01, make_float2(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1])),
@@ -714,7 +738,11 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.num_m = (int)((a.T + BM * kCta - 1) / (BM * kCta));
   p.num_n = (int)((a.N + BN - 1) / BN);
   p.w_codes = a.Wq8;
-  p.w_l2_prefetch = (kCta == 1 && !a.P_debug) ? 1 : 0;
+  static const int prefetch_env = [] {
+    const char* e = getenv("RRS_W_L2_PREFETCH");
+    return e ? atoi(e) : 0;  // off by default: no decode-step gain measured
+  }();
+  p.w_l2_prefetch = (kCta == 1 && !a.P_debug && prefetch_env) ? 1 : 0;
   p.num_mn = p.num_m * p.num_n;
   p.splits = a.splits;
   p.kps = p.KB / a.splits;

@@ -156,6 +156,7 @@ RRS_DEV void cp_async4(void* smem_dst, const void* gsrc, uint32_t src_bytes) {
 }
 RRS_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 RRS_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+RRS_DEV void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 RRS_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 RRS_DEV void bulk_wait_group_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 RRS_DEV void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
