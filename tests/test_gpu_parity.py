@@ -510,6 +510,64 @@ def test_invalid_arguments_raise():
 
 # ------------------------------------------------------------------------------------- full size, sampled
 
+def test_full_size_c3_up_sampled():
+    """The bench.py headline at full size (configs[2] up_proj: 4096 x 4096 x 14336, bf16 Y through rrs_linear,
+    the bench's launch configuration): the prologue is checked in full (oracle rotation of all 4096 tokens:
+    every s_g, alpha_t and code); Y on 48 sampled token rows x 64 sampled output features (the oracle prepares
+    only those weight rows), both against the same oracle arithmetic."""
+    w = WORKLOADS["c3_llama3_8b_up"]
+    X_bits, W_bits, Xc = make_layer(w, index=list(WORKLOADS).index("c3_llama3_8b_up"))
+    perm = _perm(Xc[:256])
+    p = torch.from_numpy(perm).to(DEV)
+    g = _run_prologue(X_bits, perm)
+    Xr = o.rotate(bf16_bits_to_f64(X_bits))
+    s = o.group_scales(o.channel_max(Xr), perm, 128)
+    q, a = o.smooth_quant(Xr, perm, s, 128)
+    assert np.array_equal(g["s_group"].view(np.uint32), s.view(np.uint32))
+    assert np.array_equal(g["alpha"].view(np.uint32), a.view(np.uint32))
+    assert np.array_equal(g["Xq8"], q)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), p)
+    Y = layer(dev_bf16(X_bits), out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    rows = rng.choice(w.T, size=48, replace=False)
+    cols = np.sort(rng.choice(w.N, size=64, replace=False))
+    qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits[cols]), perm)
+    assert np.array_equal(layer.w_scale.cpu().numpy()[cols].view(np.uint32), beta.view(np.uint32))
+    P = o.group_partials(q[rows], qw, 128)
+    Yref = o.scale_accumulate(P, s, a[rows], beta, 1.0 / w.K)
+    ref = dict(P=P, s_group=s, alpha=a[rows], beta=beta, out_scale=1.0 / w.K, Y=Yref)
+    Ys = Y.float().cpu().numpy()[np.ix_(rows, cols)]
+    assert bf16_ulp_error(Ys, Yref, ref) <= 1.0
+
+
+def test_full_size_c3_down_sampled():
+    """configs[2] down_proj at full size (4096 x 14336 x 4096, K = 28 * 512, spike-profile activations), bf16 Y
+    through rrs_linear: every code of the prologue, Y on sampled rows x columns (as above)."""
+    w = WORKLOADS["c3_llama3_8b_down"]
+    X_bits, W_bits, Xc = make_layer(w, index=list(WORKLOADS).index("c3_llama3_8b_down"))
+    perm = _perm(Xc[:256])
+    p = torch.from_numpy(perm).to(DEV)
+    g = _run_prologue(X_bits, perm)
+    Xr = o.rotate(bf16_bits_to_f64(X_bits))
+    s = o.group_scales(o.channel_max(Xr), perm, 128)
+    q, a = o.smooth_quant(Xr, perm, s, 128)
+    assert np.array_equal(g["s_group"].view(np.uint32), s.view(np.uint32))
+    assert np.array_equal(g["alpha"].view(np.uint32), a.view(np.uint32))
+    assert np.array_equal(g["Xq8"], q)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), p)
+    Y = layer(dev_bf16(X_bits), out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(2)
+    rows = rng.choice(w.T, size=48, replace=False)
+    cols = np.sort(rng.choice(w.N, size=64, replace=False))
+    qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits[cols]), perm)
+    P = o.group_partials(q[rows], qw, 128)
+    Yref = o.scale_accumulate(P, s, a[rows], beta, 1.0 / w.K)
+    ref = dict(P=P, s_group=s, alpha=a[rows], beta=beta, out_scale=1.0 / w.K, Y=Yref)
+    assert bf16_ulp_error(Y.float().cpu().numpy()[np.ix_(rows, cols)], Yref, ref) <= 1.0
+
+
 def test_full_size_c2_sampled_rows():
     """BASELINE configs[1] at full size (2048 x 4096 x 4096), same launch configuration as bench.py.
 
