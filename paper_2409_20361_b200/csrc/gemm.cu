@@ -67,6 +67,11 @@ __device__ __forceinline__ void gtrace(int, int) {}
 #ifndef RRS_GEMM_SPIN_EPI
 #define RRS_GEMM_SPIN_EPI 0
 #endif
+// 1: the 12 promotion warps of a CTA meet at a named barrier and ONE thread arrives on the leader's tempty
+// (2 arrivals per buffer per pair instead of 24, 12 of them remote); 0: every warp arrives
+#ifndef RRS_GEMM_ONE_RELEASE
+#define RRS_GEMM_ONE_RELEASE 0
+#endif
 #ifndef RRS_GEMM_SPIN_MMA
 #define RRS_GEMM_SPIN_MMA 0
 #endif
@@ -159,7 +164,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], kCta * NUM_EPI_WARPS);  // only the leader's copy is used
+      ptx::mbar_init(&tempty[b], kCta * (RRS_GEMM_ONE_RELEASE ? 1 : NUM_EPI_WARPS));  // only the leader's copy is used
     }
     ptx::fence_barrier_init();
   }
@@ -337,15 +342,23 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     // buffer releases go to the pair leader's tempty barriers
     const uint32_t tempty_addr0 = kCta == 2 ? ptx::mapa_shared(&tempty[0], 0) : ptx::smem_u32(&tempty[0]);
     const uint32_t tempty_addr1 = kCta == 2 ? ptx::mapa_shared(&tempty[1], 0) : ptx::smem_u32(&tempty[1]);
-    if (lane == 0) {
-      if constexpr (kFp8) {
-        ptx::mbar_arrive_remote(tempty_addr0);
-        ptx::mbar_arrive_remote(tempty_addr1);
-      } else {
-        ptx::mbar_arrive_cluster(tempty_addr0);
-        ptx::mbar_arrive_cluster(tempty_addr1);
+    [[maybe_unused]] const int et0 = (int)threadIdx.x - 64;
+    // release of an accumulator buffer to the pair leader's MMA thread (after this thread's tcgen05.ld/st)
+    auto release = [&](uint32_t addr) {
+      ptx::tc_fence_before();
+#if RRS_GEMM_ONE_RELEASE
+      asm volatile("bar.sync 3, %0;" ::"n"(NUM_EPI_WARPS * 32));
+      if (et0 == 0) {
+#else
+      __syncwarp();
+      if (lane == 0) {
+#endif
+        if constexpr (kFp8) ptx::mbar_arrive_remote(addr);
+        else ptx::mbar_arrive_cluster(addr);  // release at cluster scope: orders the bias re-arm tcgen05.st
       }
-    }
+    };
+    release(tempty_addr0);
+    release(tempty_addr1);
     const float2 neg_bias2 = make_float2(-12582912.0f, -12582912.0f);  // -1.5*2^23
     // eight registers holding the bias bits, the source of the re-arming tcgen05.st (kept live across the
     // loop; their value comes from shared memory so it is not re-materialised as an immediate)
@@ -432,9 +445,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
         const uint32_t tbase = tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS;
 #if defined(RRS_TRACE) && defined(RRS_GEXP) && RRS_GEXP == 1
         if constexpr (kFp8 && !kDebug) {  // timeline experiment: no TMEM readout at all
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+          release(b ? tempty_addr1 : tempty_addr0);
           acc2[g % (EPI_COLS / 2)].x += s;
         } else
 #endif
@@ -453,9 +464,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             RRS_TMEM_LD16(tbase + cc * 16, r);
             RRS_TMEM_WAIT_LD16(r);
             if (cc == EPI_COLS / 16 - 1) {  // every column of this buffer is in registers: release it
-              ptx::tc_fence_before();
-              __syncwarp();
-              if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+              release(b ? tempty_addr1 : tempty_addr0);
             }
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -491,9 +500,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             if (cc + 1 < NCH) {
               RRS_TMEM_WAIT_LD16(nxt);
               if (cc + 2 == NCH) {  // all chunks of this buffer are in registers: release it
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+                release(b ? tempty_addr1 : tempty_addr0);
                 if (trace_me) gtrace(trow, ew == 0 ? 4 : 6);
               }
             }
@@ -507,9 +514,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             if constexpr (kFp8) {
               if (cc == EPI_COLS / 16 - 1) {
                 // every column of this buffer is in registers: release it before the last chunk's math
-                ptx::tc_fence_before();
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive_remote(b ? tempty_addr1 : tempty_addr0);
+                release(b ? tempty_addr1 : tempty_addr0);
               }
             }
             if (kDebug && row < p.T) {
@@ -535,9 +540,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
 #pragma unroll
           for (int cc = 0; cc < EPI_COLS / 8; ++cc) RRS_TMEM_ST8(tbase + cc * 8, bias8);  // re-arm
           ptx::tmem_st_wait();
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive_cluster(b ? tempty_addr1 : tempty_addr0);
+          release(b ? tempty_addr1 : tempty_addr0);
         }
         ++acc_iter;
       }
