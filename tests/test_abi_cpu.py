@@ -73,3 +73,16 @@ def test_no_oracle_import_in_product_path():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(from|import)\s+oracle", txt, flags=re.M), f
                 assert "rrs_oracle" not in txt, f
+
+
+def test_flag_constants_match_header():
+    """Every RRS_* flag / status constant of the binding equals the header's #define (the marshalling layer
+    cannot drift from the C-ABI)."""
+    import re
+    from paper_2409_20361_b200 import _lib
+    hdr = open(os.path.join(ROOT, "include", "rrs.h")).read()
+    defs = {m.group(1): int(m.group(2), 16) for m in re.finditer(r"#define (RRS_[A-Z0-9_]+) (0x[0-9a-fA-F]+)u", hdr)}
+    assert {"RRS_GEMM_PLAIN", "RRS_OPERAND_I8", "RRS_TOKEN_SHARDED", "RRS_GEMM_SWIGLU", "RRS_GEMM_SUBCHANNEL"} <= set(defs)
+    for name, val in defs.items():
+        assert getattr(_lib, name) == val, name
+    assert len(set(defs.values())) == len(defs)  # distinct bits
