@@ -117,8 +117,6 @@ struct GemmParams {
   int64_t ldy;
   int32_t* P_debug;
   int y_tma;  // bf16 Y written by TMA tensor stores (16-byte aligned base, ldy % 8 == 0)
-  const int8_t* w_codes;  // Wq8 (for the decode-path L2 prefetch)
-  int w_l2_prefetch;
   int swiglu; // W rows interleaved (gate_i, up_i); Y[t][i] = bf16(silu(y_2i) * y_2i+1)
 };
 
@@ -174,20 +172,6 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   }
   if (threadIdx.x < 8) bias_sm[threadIdx.x] = 0x4B400000u;
   if constexpr (kCta == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrive / TMA
-  if constexpr (kCta == 1) {
-    // decode-sized T: the GEMM streams W (an offline input) from HBM and little else.  Under programmatic
-    // dependent launch this grid starts while the prologue still runs (it occupies few SMs at this T), so
-    // the producer warp pulls this CTA's whole W slice into L2 before waiting for the prologue's results.
-    if (p.w_l2_prefetch && warp == 2) {
-      for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
-        const int mn = tile % p.num_mn, kb0 = (tile / p.num_mn) * p.kps;
-        const int n0 = (mn / p.num_m) * BN;
-        const uint32_t bytes = (uint32_t)p.kps * BK;
-        for (int r = lane; r < BN && n0 + r < p.N; r += 32)
-          ptx::prefetch_l2_bulk(p.w_codes + (int64_t)(n0 + r) * p.K + (int64_t)kb0 * BK, bytes);
-      }
-    }
-  }
   ptx::pdl_wait();  // Xq8 / x_scale / s_group come from the prologue kernels (programmatic dependent launch)
   if (!kPlain && p.s_group) {
     for (int g = threadIdx.x; g < p.G; g += blockDim.x) s_sm[g] = p.s_group[g];
@@ -740,12 +724,6 @@ static cudaError_t launch_cta(const GemmArgs& a, int nsm, cudaStream_t st) {
   p.gk = a.group / 32;
   p.num_m = (int)((a.T + BM * kCta - 1) / (BM * kCta));
   p.num_n = (int)((a.N + BN - 1) / BN);
-  p.w_codes = a.Wq8;
-  static const int prefetch_env = [] {
-    const char* e = getenv("RRS_W_L2_PREFETCH");
-    return e ? atoi(e) : 0;  // off by default: no decode-step gain measured
-  }();
-  p.w_l2_prefetch = (kCta == 1 && !a.P_debug && prefetch_env) ? 1 : 0;
   p.num_mn = p.num_m * p.num_n;
   p.splits = a.splits;
   p.kps = p.KB / a.splits;

@@ -86,3 +86,23 @@ def test_flag_constants_match_header():
     for name, val in defs.items():
         assert getattr(_lib, name) == val, name
     assert len(set(defs.values())) == len(defs)  # distinct bits
+
+
+def test_hot_kernels_do_not_spill(lib_path):
+    """The bench-path kernels keep everything in registers (STACK 0): a 24-byte spill in the RRS GEMM once cost
+    4 % of its time after an unrelated change moved ptxas's register allocation."""
+    out = subprocess.run(["cuobjdump", "-res-usage", lib_path], capture_output=True, text=True).stdout
+    hot = ["rrs_gemm_kernelILb0ELb0ELb0ELi2ELb1ELb0E",   # RRS GEMM, bf16 Y, CTA pairs, E4M3 (the headline)
+           "rrs_gemm_kernelILb1ELb0ELb0ELi2ELb1ELb0E",   # plain per-channel baseline
+           "fwht_colmax_kernelILi14336E", "smooth_quant_kernelILi14336E", "smooth_quant_kernelILi4096E"]
+    usage = {}
+    lines = out.splitlines()
+    for i, l in enumerate(lines):
+        m = re.search(r"Function (\S+):", l)
+        if m and i + 1 < len(lines):
+            usage[m.group(1)] = lines[i + 1]
+    for h in hot:
+        names = [n for n in usage if h in n]
+        assert names, h
+        for n in names:
+            assert "STACK:0 " in usage[n] and "LOCAL:0 " in usage[n], (n, usage[n])
