@@ -299,13 +299,15 @@ def test_swiglu_epilogue_tma_width():
     assert bf16_ulp_error(Hn[:T, :F], o.swiglu(Y[:, 0::2], Y[:, 1::2])) <= 1.0
 
 
-@pytest.mark.parametrize("T,N,K,out", [(1, 1024, 8192, "f32"), (17, 1024, 8192, "bf16"), (64, 488, 8192, "f32"),
-                                       (100, 520, 14336, "f32"), (128, 264, 4096, "bf16")])
-def test_decode_split_k(T, N, K, out):
+@pytest.mark.parametrize("T,N,K,out,i8", [(1, 1024, 8192, "f32", False), (17, 1024, 8192, "bf16", False),
+                                          (64, 488, 8192, "f32", False), (100, 520, 14336, "f32", False),
+                                          (128, 264, 4096, "bf16", False), (33, 512, 8192, "f32", True),
+                                          (5, 264, 2048, "bf16", True)])
+def test_decode_split_k(T, N, K, out, i8):
     """Decode-sized T (<= 128, configs[3]): rrs_linear splits K over up to 8 CTAs per output tile (whole groups
     each) and sums the f32 partials in a fixed order -- same bar against the oracle, deterministic."""
     X_bits, W_bits, perm, ref = _gemm_case(T, N, K, "mixed", seed=T)
-    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV))
+    layer = rrs.RRSLinear(dev_bf16(W_bits), torch.from_numpy(perm).to(DEV), i8=i8)
     X = dev_bf16(X_bits)
     if out == "f32":
         Y = layer(X, out_dtype=torch.float32)
@@ -349,19 +351,20 @@ def test_subchannel_gemm_baseline(T, N, K, group, out):
         assert np.all(np.abs(Y.float().cpu().numpy().astype(np.float64) - ref_b) <= ulp + 1e-5 * den)
 
 
-def test_swiglu_epilogue():
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_swiglu_epilogue(i8):
     """RRS_GEMM_SWIGLU: with interleaved (gate, up) rows the bf16 output is, within 1 bf16 ulp,
     bf16(silu(y_2i) * y_2i+1) of the very same GEMM's f32 output (the epilogue math is f32: one f32 product with
     beta, e^-g and a division), and that f32 output meets the §5 bar against the oracle."""
     T, F, K = 257, 260, 4096
     X_bits, W_bits, perm, ref = _gemm_case(T, 2 * F, K, "mixed", seed=7)
-    Xq8 = _dev(encode_operand(ref["q"], False))
-    Wq8 = _dev(encode_operand(ref["qw"], False))
+    Xq8 = _dev(encode_operand(ref["q"], i8))
+    Wq8 = _dev(encode_operand(ref["qw"], i8))
     xs, sg, ws = (torch.from_numpy(ref[k]).to(DEV) for k in ("alpha", "s_group", "beta"))
     Yf = torch.empty((T, 2 * F), dtype=torch.float32, device=DEV)
-    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf, 1.0 / K)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, Yf, 1.0 / K, i8=i8)
     H = torch.full((T, F + 4), float("nan"), dtype=torch.bfloat16, device=DEV)
-    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, H[:, :F], 1.0 / K, swiglu=True)
+    rrs.rrs_gemm(Xq8, xs, sg, Wq8, ws, H[:, :F], 1.0 / K, swiglu=True, i8=i8)
     torch.cuda.synchronize()
     Y = Yf.cpu().numpy().astype(np.float64)
     assert y_normalised_error(Yf.cpu().numpy(), ref) <= 1e-5
@@ -448,8 +451,8 @@ def test_comm_world1_path_equals_single_gpu():
         rrs.rrs_comm_destroy(comm)
 
 
-@pytest.mark.parametrize("K,T", [(4096, 200), (14336, 70), (1024, 0)])
-def test_token_sharded_world1_equals_single_gpu(K, T):
+@pytest.mark.parametrize("K,T,i8", [(4096, 200, False), (14336, 70, False), (1024, 0, False), (2048, 150, True)])
+def test_token_sharded_world1_equals_single_gpu(K, T, i8):
     """Token-sharded data parallel (RRS_TOKEN_SHARDED) with a 1-rank communicator: the two-pass
     prologue + ncclAllReduce(MAX) of chan_max + GEMM equals the single-GPU layer (fused prologue for 2^m)
     bit for bit; T = 0 still joins the collective."""
@@ -460,8 +463,8 @@ def test_token_sharded_world1_equals_single_gpu(K, T):
     comm = rrs.rrs_comm_init(0, 1, uid)
     try:
         p = torch.from_numpy(perm).to(DEV)
-        single = rrs.RRSLinear(dev_bf16(W_bits), p)
-        dp = rrs.RRSLinear(dev_bf16(W_bits), p, comm=comm, world=1, rank=0, token_sharded=True)
+        single = rrs.RRSLinear(dev_bf16(W_bits), p, i8=i8)
+        dp = rrs.RRSLinear(dev_bf16(W_bits), p, comm=comm, world=1, rank=0, token_sharded=True, i8=i8)
         X = dev_bf16(X_bits)
         a = single(X, out_dtype=torch.float32)
         b = dp(X, out_dtype=torch.float32)
