@@ -80,6 +80,9 @@ int rrs_version(void);
  * pass) + chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xop[T][K] u8 (+ Y shard and gather
  * buffers when world > 1), each 256-byte aligned.  Returns 0 for invalid arguments. */
 size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world);
+/* Workspace for rrs_linear / rrs_allgather_columns WITH a communicator of `world` ranks (world >= 1; a 1-rank
+ * communicator still runs the NCCL path): as above plus the Y shard and all-gather buffers, always. */
+size_t rrs_workspace_bytes_comm(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world);
 
 /* Offline reorder helper ("reorder the activations and weights according to the magnitude
  * of smoothing scales"; R5, R21): perm[j'] = channel of rank j' when channels are sorted by

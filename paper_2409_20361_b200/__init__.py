@@ -12,7 +12,8 @@ import torch
 
 from ._lib import (EXPORTS, RRSError, lib, rrs_allgather_columns, rrs_comm_destroy, rrs_comm_init, rrs_comm_unique_id,  # noqa: F401
                    rrs_debug_group_partials, rrs_debug_rotate, rrs_gemm, rrs_linear, rrs_perm_from_channel_max,
-                   rrs_prepare_weights, rrs_rotate_smooth_quant, rrs_version, rrs_workspace_bytes)
+                   rrs_prepare_weights, rrs_rotate_smooth_quant, rrs_version, rrs_workspace_bytes,
+                   rrs_workspace_bytes_comm)
 
 GROUP = 128
 
@@ -63,7 +64,10 @@ class RRSLinear:
         self._ws = None
 
     def workspace(self, T: int, device) -> torch.Tensor:
-        need = rrs_workspace_bytes(T, self.N_total, self.K, self.group, 1 if self.token_sharded else self.world)
+        if self.comm is not None and not self.token_sharded:  # column-parallel: shard + all-gather buffers
+            need = rrs_workspace_bytes_comm(T, self.N_total, self.K, self.group, self.world)
+        else:
+            need = rrs_workspace_bytes(T, self.N_total, self.K, self.group, 1)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=device)
         return self._ws

@@ -31,6 +31,7 @@ _SIGS = {
     "rrs_last_error": (ctypes.c_char_p, []),
     "rrs_version": (ctypes.c_int, []),
     "rrs_workspace_bytes": (_c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32]),
+    "rrs_workspace_bytes_comm": (_c_sz, [_c_i64, _c_i64, _c_i64, _c_i32, _c_i32]),
     "rrs_perm_from_channel_max": (ctypes.c_int, [_c_p, _c_i64, _c_p, _c_p]),
     "rrs_prepare_weights": (ctypes.c_int, [_c_p, _c_i32, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_u32,
                                            _c_p]),
@@ -122,6 +123,11 @@ def rrs_version() -> int:
 
 def rrs_workspace_bytes(T: int, N: int, K: int, group: int = 128, world: int = 1) -> int:
     return int(lib().rrs_workspace_bytes(T, N, K, group, world))
+
+
+def rrs_workspace_bytes_comm(T: int, N: int, K: int, group: int = 128, world: int = 1) -> int:
+    """Workspace for rrs_linear with a communicator of `world` ranks (shard + all-gather buffers included)."""
+    return int(lib().rrs_workspace_bytes_comm(T, N, K, group, world))
 
 
 def rrs_perm_from_channel_max(chan_max, perm, stream=None) -> None:

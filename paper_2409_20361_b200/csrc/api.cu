@@ -102,7 +102,9 @@ struct Workspace {
 constexpr int kMaxSplits = 8;
 constexpr int64_t kSplitMaxT = 128;  // the single-CTA (M = 128) GEMM regime
 
-size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t world, Workspace* w) {
+// gather_world: ranks of the column-parallel communicator whose shard / gather buffers are carved (0 = none)
+size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t gather_world, Workspace* w) {
+  const int32_t world = gather_world;
   size_t off = 0;
   auto take = [&](size_t bytes) -> void* {
     void* p = base ? static_cast<char*>(base) + off : nullptr;
@@ -119,7 +121,7 @@ size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t
   ws.y_shard = nullptr;
   ws.y_gather = nullptr;
   ws.part = (T > 0 && T <= kSplitMaxT) ? static_cast<float*>(take(sizeof(float) * kMaxSplits * (size_t)T * N)) : nullptr;
-  if (world > 1) {
+  if (world >= 1) {
     const int64_t ns = N / world;
     ws.y_shard = take((size_t)T * ns * 4);
     ws.y_gather = take((size_t)T * N * 4);
@@ -132,7 +134,10 @@ size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t
 struct rrs_comm_s {
   ncclComm_t nccl;
   int rank, world;
+  cudaStream_t side = nullptr;  // all-gather + relayout of GEMM token slabs, overlapping the next slab's GEMM
+  cudaEvent_t ev[9] = {};       // [0..7] slab GEMM done, [8] side stream done
 };
+constexpr int kMaxSlabs = 8;
 
 static rrs_status gather_columns(const void* shard, int64_t T, int64_t N_total, int esz, void* Y, int64_t ldy,
                                  rrs_comm_t comm, void* gather_buf, cudaStream_t st) {
@@ -195,6 +200,11 @@ int rrs_version(void) { return 100; }
 
 size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world) {
   if (T < 0 || K <= 0 || group <= 0 || K % group || world < 1 || (world > 1 && (N <= 0 || N % world))) return 0;
+  return carve(nullptr, T, N, K, group, world > 1 ? world : 0, nullptr);
+}
+
+size_t rrs_workspace_bytes_comm(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world) {
+  if (T < 0 || K <= 0 || group <= 0 || K % group || world < 1 || N <= 0 || N % world) return 0;
   return carve(nullptr, T, N, K, group, world, nullptr);
 }
 
@@ -277,7 +287,7 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
   if (!aligned16(X) || !aligned16(perm) || !aligned16(Xq) || !aligned16(Xq8))
     return fail(RRS_ERR_MISALIGNED, "pointers must be 16-byte aligned");
   Workspace w;
-  const size_t need = carve(ws, T, 1, K, group, 1, &w);
+  const size_t need = carve(ws, T, 1, K, group, 0, &w);
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   if (!chan_max) chan_max = w.chan_max;
@@ -365,7 +375,7 @@ static rrs_status linear_token_sharded(const void* X, int64_t T, int64_t K, int3
   if ((T > 0 && !X) || !perm) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
   Workspace w;
-  const size_t need = carve(ws, T, N, K, group, 1, &w);
+  const size_t need = carve(ws, T, N, K, group, 0, &w);
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   if (T > 0)
@@ -409,7 +419,7 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if ((T > 0 && !X) || !perm) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
   if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
   Workspace w;
-  const size_t need = carve(ws, T, N_total, K, group, world, &w);
+  const size_t need = carve(ws, T, N_total, K, group, comm ? world : 0, &w);
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -419,7 +429,7 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (T == 0) return RRS_OK;
   const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
   const int esz = y_dtype == RRS_F32 ? 4 : 2;
-  if (world == 1) {
+  if (!comm) {
     if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy, swiglu)) return s;
     rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N_total, K, group, out_scale, false, e4m3, Y,
                     y_dtype, ldy, nullptr, swiglu};
@@ -432,11 +442,34 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, n_local, K, group, w.y_shard, n_out_local, swiglu))
     return s;
   if (ldy < n_out || !aligned16(Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "Y / ldy");
-  rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, n_local, K, group, out_scale, false, e4m3,
-                  w.y_shard, y_dtype, n_out_local, nullptr, swiglu};
-  cudaError_t e = rrs::launch_gemm(a, nsm, st);
-  if (e != cudaSuccess) return cuda_fail(e, "rrs_gemm kernel");
-  return gather_columns(w.y_shard, T, n_out, esz, Y, ldy, comm, w.y_gather, st);
+  if ((n_out_local * esz) % 16 || (ldy * esz) % 16)
+    return fail(RRS_ERR_MISALIGNED, "shard width and ldy must be multiples of 16 bytes");
+  // Token slabs (SURVEY §8(e) "overlap by token slabs"): the GEMM of slab s runs on `st` while the all-gather
+  // and relayout of slab s-1 run on the communicator's side stream, so the NVLink transfer overlaps compute.
+  // Slabs are whole 256-row M-blocks of the pair GEMM; the shard / gather buffers are laid out slab-major.
+  const int64_t rows = T >= 1024 ? (((T + 3) / 4 + 255) / 256) * 256 : T;
+  const int nslab = (int)((T + rows - 1) / rows);
+  if (nslab > kMaxSlabs) return fail(RRS_ERR_INVALID_ARGUMENT, "too many slabs");
+  cudaError_t e = cudaEventRecord(comm->ev[8], st);  // the side stream starts after the prologue (and whatever
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(comm->side, comm->ev[8], 0);  // came before it on st)
+  if (e != cudaSuccess) return cuda_fail(e, "slab pipeline ordering");
+  for (int sl = 0; sl < nslab; ++sl) {
+    const int64_t t0 = sl * rows, ts = std::min(rows, T - t0);
+    char* shard = static_cast<char*>(w.y_shard) + t0 * n_out_local * esz;
+    rrs::GemmArgs a{w.Xq8 + t0 * K, w.x_scale + t0, w.s_group, Wq8, w_scale, ts, n_local, K, group, out_scale, false,
+                    e4m3, shard, y_dtype, n_out_local, nullptr, swiglu};
+    e = rrs::launch_gemm(a, nsm, st);
+    if (e != cudaSuccess) return cuda_fail(e, "rrs_gemm kernel");
+    e = cudaEventRecord(comm->ev[sl], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(comm->side, comm->ev[sl], 0);
+    if (e != cudaSuccess) return cuda_fail(e, "slab event");
+    if (rrs_status s = gather_columns(shard, ts, n_out, esz, static_cast<char*>(Y) + t0 * ldy * esz, ldy, comm,
+                                      static_cast<char*>(w.y_gather) + t0 * n_out * esz, comm->side))
+      return s;
+  }
+  e = cudaEventRecord(comm->ev[8], comm->side);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(st, comm->ev[8], 0);  // Y complete in stream order on st
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "slab pipeline join");
 }
 
 rrs_status rrs_allgather_columns(const void* Y_shard, int64_t T, int64_t N_total, int32_t y_dtype, void* Y,
@@ -480,6 +513,13 @@ rrs_status rrs_comm_init(rrs_comm_t* comm, int32_t rank, int32_t world, const ui
   }
   c->rank = rank;
   c->world = world;
+  cudaError_t e = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+  for (int i = 0; i < 9 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    ncclCommDestroy(c->nccl);
+    delete c;
+    return cuda_fail(e, "side stream / events for the slab pipeline");
+  }
   *comm = c;
   return RRS_OK;
 }
@@ -488,6 +528,9 @@ rrs_status rrs_comm_destroy(rrs_comm_t comm) {
   g_last_error.clear();
   if (!comm) return RRS_OK;
   ncclResult_t r = ncclCommDestroy(comm->nccl);
+  for (int i = 0; i < 9; ++i)
+    if (comm->ev[i]) cudaEventDestroy(comm->ev[i]);
+  if (comm->side) cudaStreamDestroy(comm->side);
   delete comm;
   return r == ncclSuccess ? RRS_OK : fail(RRS_ERR_NCCL, "ncclCommDestroy: %s", ncclGetErrorString(r));
 }
