@@ -143,7 +143,10 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
  * comm == NULL: single GPU, Wop/w_scale hold all N rows.
  * comm != NULL (column-parallel): Wop/w_scale hold THIS rank's N/world output rows
  *   [rank*N/world, (rank+1)*N/world); X is replicated; every rank runs the identical prologue; Y
- *   receives all N columns through an NCCL all-gather.  N_total % world == 0 required.
+ *   receives all N columns through an NCCL all-gather (any world >= 1; ws sized by rrs_workspace_bytes_comm).
+ *   For T >= 1024 the GEMM runs in 256-row-aligned token slabs whose all-gathers run on an internal stream
+ *   of the communicator, overlapping the next slab's GEMM; Y is complete in `stream` order on return.
+ *   N_total % world == 0 required.
  * comm != NULL and flags & RRS_TOKEN_SHARDED (data parallel over tokens): X holds THIS
  *   rank's T tokens (T may differ between ranks, 0 included), Wop/w_scale hold all N_total rows, Y
  *   receives this rank's [T][N_total].  The runtime channel max is over ALL tokens of the call (Eq. 1
