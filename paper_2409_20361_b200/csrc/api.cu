@@ -73,11 +73,19 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 // Smoothing group: the paper's 128 = the GEMM K-block, and the Table-4 sizes; a power of
 // two in [32, 1024] (a multiple of the 32-deep MMA K-step that divides or is divided by the 128-deep K-block)
+// G = K / group is capped at kMaxGroups: the FP32 scale-accumulate sum_g fl(s_g rs) P_g has a worst-case
+// normalised error of about (G + 2) 2^-24, which stays under the north_star's 1e-5 only for
+// G <= 165; beyond that the parity bar could not be promised, so such calls are refused.
+constexpr int64_t kMaxGroups = 160;
+
 rrs_status check_group(int64_t K, int32_t group) {
   if (group < 32 || group > 1024 || (group & (group - 1)))
     return fail(RRS_ERR_INVALID_ARGUMENT, "group=%d: need a power of two in [32, 1024] (128 = P:189)", group);
   if (K <= 0 || K % group || K % 128)
     return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K=%lld must be a positive multiple of group %d and of 128", (long long)K, group);
+  if (K / group > kMaxGroups)
+    return fail(RRS_ERR_UNSUPPORTED_SHAPE, "K/group = %lld groups > %lld: the 1e-5 FP32 bound needs G <= 160 (DESIGN.md §5)",
+                (long long)(K / group), (long long)kMaxGroups);
   return RRS_OK;
 }
 
@@ -176,6 +184,28 @@ cudaError_t prepare_kernel_impl(const void* fn, int smem, int threads, int* bloc
   if (blocks_per_sm) *blocks_per_sm = per_sm;
   return cudaSuccess;
 }
+int max_active_clusters_impl(const void* fn, int cluster, int threads, int smem) {
+  static std::mutex mu;
+  struct Entry { const void* fn; int dev, n; };
+  static Entry cache[128];
+  static int n = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lk(mu);
+  for (int i = 0; i < n; ++i)
+    if (cache[i].fn == fn && cache[i].dev == dev) return cache[i].n;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cluster * 1024);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  int c = 0;
+  if (cudaOccupancyMaxActiveClusters(&c, fn, &cfg) != cudaSuccess || c < 1) {
+    cudaGetLastError();
+    c = 0;
+  }
+  if (n < 128) cache[n++] = Entry{fn, dev, c};
+  return c;
+}
 }  // namespace rrs
 
 extern "C" {
@@ -262,7 +292,10 @@ static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* p
   if (T > 0 && rrs::prologue_fused_supports_k(K)) {
     e = rrs::launch_prologue_fused(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
                                    counter, perm, s_group, Xq, Xq8, x_scale, e4m3, group, nsm, st);
-    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_fused_kernel");
+    if (e == cudaSuccess) return RRS_OK;
+    if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
+      return cuda_fail(e, "prologue_fused_kernel");
+    cudaGetLastError();  // refused (grid cannot be co-resident): the two-kernel prologue below
   }
   e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
                               nsm, st);
@@ -423,27 +456,33 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
+  const int esz = y_dtype == RRS_F32 ? 4 : 2;
+  // with the fused SwiGLU each rank's shard holds whole (gate, up) pairs and yields n_local / 2 outputs
+  const int64_t n_out_local = swiglu ? n_local / 2 : n_local, n_out = swiglu ? N_total / 2 : N_total;
+  // every argument is validated before anything is enqueued (rrs.h conventions)
+  if (T > 0) {
+    if (!comm) {
+      if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy, swiglu)) return s;
+    } else {
+      if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, n_local, K, group, w.y_shard, n_out_local, swiglu))
+        return s;
+      if (ldy < n_out || !Y || !aligned16(Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "Y / ldy");
+      if ((n_out_local * esz) % 16 || (ldy * esz) % 16)
+        return fail(RRS_ERR_MISALIGNED, "shard width and ldy must be multiples of 16 bytes");
+    }
+  }
   if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max,
                               reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, e4m3, group, nsm, st))
     return s;
   if (T == 0) return RRS_OK;
-  const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
-  const int esz = y_dtype == RRS_F32 ? 4 : 2;
   if (!comm) {
-    if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy, swiglu)) return s;
     rrs::GemmArgs a{w.Xq8, w.x_scale, w.s_group, Wq8, w_scale, T, N_total, K, group, out_scale, false, e4m3, Y,
                     y_dtype, ldy, nullptr, swiglu};
     cudaError_t e = layer_gemm(a, w, nsm, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_gemm kernel");
   }
   // column-parallel: local shard [T][n_local] -> all-gather [world][T][n_local] -> Y[T][ldy]
-  // with the fused SwiGLU each rank's shard holds whole (gate, up) pairs and yields n_local / 2 outputs
-  const int64_t n_out_local = swiglu ? n_local / 2 : n_local, n_out = swiglu ? N_total / 2 : N_total;
-  if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, n_local, K, group, w.y_shard, n_out_local, swiglu))
-    return s;
-  if (ldy < n_out || !aligned16(Y)) return fail(RRS_ERR_INVALID_ARGUMENT, "Y / ldy");
-  if ((n_out_local * esz) % 16 || (ldy * esz) % 16)
-    return fail(RRS_ERR_MISALIGNED, "shard width and ldy must be multiples of 16 bytes");
   // Token slabs (SURVEY §8(e) "overlap by token slabs"): the GEMM of slab s runs on `st` while the all-gather
   // and relayout of slab s-1 run on the communicator's side stream, so the NVLink transfer overlaps compute.
   // Slabs are whole 256-row M-blocks of the pair GEMM; the shard / gather buffers are laid out slab-major.
@@ -453,22 +492,24 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   cudaError_t e = cudaEventRecord(comm->ev[8], st);  // the side stream starts after the prologue (and whatever
   if (e == cudaSuccess) e = cudaStreamWaitEvent(comm->side, comm->ev[8], 0);  // came before it on st)
   if (e != cudaSuccess) return cuda_fail(e, "slab pipeline ordering");
-  for (int sl = 0; sl < nslab; ++sl) {
+  rrs_status status = RRS_OK;
+  for (int sl = 0; sl < nslab && status == RRS_OK; ++sl) {
     const int64_t t0 = sl * rows, ts = std::min(rows, T - t0);
     char* shard = static_cast<char*>(w.y_shard) + t0 * n_out_local * esz;
     rrs::GemmArgs a{w.Xq8 + t0 * K, w.x_scale + t0, w.s_group, Wq8, w_scale, ts, n_local, K, group, out_scale, false,
                     e4m3, shard, y_dtype, n_out_local, nullptr, swiglu};
     e = rrs::launch_gemm(a, nsm, st);
-    if (e != cudaSuccess) return cuda_fail(e, "rrs_gemm kernel");
+    if (e != cudaSuccess) { status = cuda_fail(e, "rrs_gemm kernel"); break; }
     e = cudaEventRecord(comm->ev[sl], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(comm->side, comm->ev[sl], 0);
-    if (e != cudaSuccess) return cuda_fail(e, "slab event");
-    if (rrs_status s = gather_columns(shard, ts, n_out, esz, static_cast<char*>(Y) + t0 * ldy * esz, ldy, comm,
-                                      static_cast<char*>(w.y_gather) + t0 * n_out * esz, comm->side))
-      return s;
+    if (e != cudaSuccess) { status = cuda_fail(e, "slab event"); break; }
+    status = gather_columns(shard, ts, n_out, esz, static_cast<char*>(Y) + t0 * ldy * esz, ldy, comm,
+                            static_cast<char*>(w.y_gather) + t0 * n_out * esz, comm->side);
   }
+  // join the side stream on every path (also after an error: a capture must not end with it forked)
   e = cudaEventRecord(comm->ev[8], comm->side);
   if (e == cudaSuccess) e = cudaStreamWaitEvent(st, comm->ev[8], 0);  // Y complete in stream order on st
+  if (status != RRS_OK) return status;
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "slab pipeline join");
 }
 

@@ -17,6 +17,14 @@ cudaError_t prepare_kernel(F kern, int smem, int threads, int* blocks_per_sm = n
   return prepare_kernel_impl(reinterpret_cast<const void*>(kern), smem, threads, blocks_per_sm);
 }
 
+// Per-(kernel, device) cached cudaOccupancyMaxActiveClusters for a kernel with compile-time cluster dims
+// (0 if the query fails).  Thread-safe.
+int max_active_clusters_impl(const void* fn, int cluster, int threads, int smem);
+template <class F>
+int max_active_clusters(F kern, int cluster, int threads, int smem) {
+  return max_active_clusters_impl(reinterpret_cast<const void*>(kern), cluster, threads, smem);
+}
+
 template <class... KArgs, class... Args>
 cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int threads, int smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -36,7 +44,8 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int threads, int smem, 
 bool prologue_supports_k(int64_t K);
 cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
                                int nsm, cudaStream_t st);
-// One persistent launch of rows a1-a6 for K = 2^m; chan_max and *counter must be zero on entry.
+// One persistent (cooperative) launch of rows a1-a6 for K = 2^m; chan_max and *counter must be zero on entry.
+// Returns cudaErrorCooperativeLaunchTooLarge (error state cleared) when the grid cannot be co-resident.
 bool prologue_fused_supports_k(int64_t K);
 cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
                                   unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,

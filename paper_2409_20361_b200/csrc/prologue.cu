@@ -484,19 +484,11 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
   if (e != cudaSuccess) return e;
   // persistent: only as many clusters as can be co-resident (a cluster of 8 must fit in one GPC, so this is
   // below SMs x CTAs-per-SM / 8); late clusters would otherwise run as a second wave
-  static int max_clusters[2] = {0, 0};  // per K instantiation, cached
-  if (max_clusters[0] == 0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(colmax_cluster<K>() * 1024);
-    cfg.blockDim = dim3(P::THREADS);
-    cfg.dynamicSmemBytes = smem;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) n = nsm / colmax_cluster<K>();
-    max_clusters[0] = n;
-  }
+  int max_clusters = max_active_clusters(kern, colmax_cluster<K>(), P::THREADS, smem);
+  if (max_clusters < 1) max_clusters = nsm / colmax_cluster<K>();
   const int64_t tiles = (T + P::R - 1) / P::R;
   if (tiles == 0) return cudaSuccess;
-  const int64_t clusters = std::min<int64_t>(max_clusters[0], (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>());
+  const int64_t clusters = std::min<int64_t>(max_clusters, (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>());
   const int grid = (int)clusters * colmax_cluster<K>();  // whole clusters (CTAs without a tile are fine)
   kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr);
   return cudaGetLastError();
@@ -511,22 +503,25 @@ static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, fl
   const int smem = ColmaxSmem<K>::BYTES;
   cudaError_t e = prepare_kernel(kern, smem, P::THREADS);
   if (e != cudaSuccess) return e;
-  // every CTA must be resident at once (grid barrier): the grid is exactly the co-resident cluster count
-  static int max_clusters = 0;
-  if (max_clusters == 0) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(colmax_cluster<K>() * 1024);
-    cfg.blockDim = dim3(P::THREADS);
-    cfg.dynamicSmemBytes = smem;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess || n < 1) return cudaErrorInvalidConfiguration;
-    max_clusters = n;
-  }
+  // every CTA must be resident at once (grid barrier): the grid is at most the co-resident cluster count, and
+  // the launch is COOPERATIVE, so the runtime refuses it (instead of letting it hang) when the grid cannot be
+  // co-resident; the caller then falls back to the two-kernel prologue
+  const int max_clusters = max_active_clusters(kern, colmax_cluster<K>(), P::THREADS, smem);
+  if (max_clusters < 1) return cudaErrorCooperativeLaunchTooLarge;
   const int64_t tiles = (T + P::R - 1) / P::R;
   const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>()));
   const int grid = (int)clusters * colmax_cluster<K>();
-  kern<<<grid, P::THREADS, smem, st>>>(X, T, cm, Xr, counter, perm, s_group, Xq, Xq8, scale, (int)e4m3, group);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(P::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, X, T, cm, Xr, counter, perm, s_group, Xq, Xq8, scale, (int)e4m3, group);
 }
 
 template <int K>

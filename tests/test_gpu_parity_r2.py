@@ -1,0 +1,179 @@
+"""Round-2 GPU parity cases (VERDICT r1 "What's weak" 2): the advertised K extremes through the whole layer,
+adversarial exactness of the FP8 carrier's FP32 tensor-core accumulation beyond |P| < 2^13, the group-count
+cap, and the full-size headline checked on whole output rows.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2409_20361_b200 as rrs  # noqa: E402
+from oracle import rrs_oracle as o  # noqa: E402
+from rrs_synth import WORKLOADS, bf16_bits_to_f64, make_activations, make_layer, make_weights  # noqa: E402
+
+from _parity import (bf16_ulp_error, decode_operand, dev_bf16, encode_operand, oracle_layer,  # noqa: E402
+                     y_normalised_error)
+
+DEV = "cuda"
+
+
+def _perm(Xc_bits):
+    return o.calibrate_perm(bf16_bits_to_f64(Xc_bits)).astype(np.int32)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+
+
+# --------------------------------------------------------------------------- K = 128 and K = 16384 end to end
+
+@pytest.mark.parametrize("K,T,N,profile", [(128, 37, 200, "channel"), (128, 300, 64, "tiny"),
+                                           (16384, 70, 264, "spike"), (16384, 129, 96, "mixed")])
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_prologue_and_layer_at_K_extremes(K, T, N, profile, i8):
+    """rrs.h advertises K in {128, ..., 16384}: the fused prologue (every code, alpha, s_g bit-exact) and the
+    whole rrs_linear layer (Y within the DESIGN.md §5 tolerance) at both ends of the range."""
+    X_bits = make_activations(profile, T, K, 1700 + K % 97, 1701)
+    W_bits = make_weights(N, K, 1702)
+    perm = _perm(make_activations(profile, 64, K, 1700 + K % 97, 1703))
+    ref = oracle_layer(X_bits, W_bits, perm)
+    X = dev_bf16(X_bits)
+    p = _dev(perm)
+    Xq = torch.empty((T, K // 2), dtype=torch.uint8, device=DEV)
+    Xop = torch.empty((T, K), dtype=torch.uint8, device=DEV)
+    xs = torch.empty(T, dtype=torch.float32, device=DEV)
+    sg = torch.empty(K // 128, dtype=torch.float32, device=DEV)
+    cm = torch.empty(K, dtype=torch.float32, device=DEV)
+    rrs.rrs_rotate_smooth_quant(X, p, Xq, Xop, xs, sg, chan_max=cm, i8=i8)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), p, keep_packed=True, i8=i8)
+    Y = layer(X, out_dtype=torch.float32)
+    Yb = layer(X, out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    assert np.array_equal(cm.cpu().numpy().view(np.uint32), ref["chan_max"].view(np.uint32))
+    assert np.array_equal(sg.cpu().numpy().view(np.uint32), ref["s_group"].view(np.uint32))
+    assert np.array_equal(xs.cpu().numpy().view(np.uint32), ref["alpha"].view(np.uint32))
+    assert np.array_equal(Xq.cpu().numpy(), ref["Xq"])
+    assert np.array_equal(decode_operand(Xop.cpu().numpy(), i8), ref["q"])
+    assert np.array_equal(layer.Wq.cpu().numpy(), ref["Wq"])
+    assert y_normalised_error(Y.cpu().numpy(), ref) <= 1e-5
+    assert bf16_ulp_error(Yb.float().cpu().numpy(), ref["Y"], ref) <= 1.0
+
+
+# --------------------------------------------------------------------------- FP8 carrier exactness, adversarial
+
+def _adversarial_codes(rows, K, L, rng, big_first):
+    """Per group of L codes: a run of +-7 codes (all rows share the run positions) that makes the partial sum
+    large, and +-1 / 0 codes elsewhere that make its low bits odd -- a tensor-core accumulator that kept fewer
+    than log2(49 L) + 1 significant bits would lose them.  big_first: the large run opens the group (the small
+    terms are then added to a large running sum) or closes it."""
+    q = rng.integers(-1, 2, size=(rows, K)).astype(np.int8)
+    for g in range(K // L):
+        run = slice(g * L, g * L + L // 2) if big_first else slice(g * L + L // 2, (g + 1) * L)
+        q[:, run] = 7
+    return q
+
+
+@pytest.mark.parametrize("L,K", [(1024, 2048), (512, 2048), (256, 1024)])
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_group_partials_adversarial_large_groups(L, K, i8):
+    """Every (t, n) pair adversarial: |P_g| up to 49 L / 2 + L / 2 (25,600 at L = 1024, > 2^14) with an odd
+    residue; P_g read back from TMEM must equal the oracle's integer sums exactly."""
+    rng = np.random.default_rng(L + K)
+    T, N = 130, 248
+    q = np.vstack([_adversarial_codes(T // 2, K, L, rng, True), _adversarial_codes(T - T // 2, K, L, rng, False)])
+    qw = np.vstack([_adversarial_codes(N // 2, K, L, rng, True), _adversarial_codes(N - N // 2, K, L, rng, False)])
+    qw[1::2] *= -1  # both signs of the large run
+    P = torch.empty((K // L, T, N), dtype=torch.int32, device=DEV)
+    rrs.rrs_debug_group_partials(_dev(encode_operand(q, i8)), _dev(encode_operand(qw, i8)), P, group=L, i8=i8)
+    torch.cuda.synchronize()
+    ref = o.group_partials(q, qw, L)
+    assert np.abs(ref).max() > 2 ** 14
+    assert (ref % 2 != 0).any()
+    assert np.array_equal(P.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("K", [14336, 16384])
+@pytest.mark.parametrize("i8", [False, True], ids=["e4m3", "i8"])
+def test_plain_gemm_exact_integer_sums_full_K(K, i8):
+    """RRS_GEMM_PLAIN (one accumulation over all K, the per-channel baseline of P:322) with alpha = beta =
+    out_scale = 1 and f32 Y: Y must be the exact integer sum_k q qw, |sum| up to 49 K / 2 + K / 2 > 2^18, with
+    odd residues added after (and before) the large run."""
+    rng = np.random.default_rng(K)
+    T, N = 136, 256
+    q = np.vstack([_adversarial_codes(T // 2, K, K, rng, True), _adversarial_codes(T - T // 2, K, K, rng, False)])
+    qw = np.vstack([_adversarial_codes(N // 2, K, K, rng, True), _adversarial_codes(N - N // 2, K, K, rng, False)])
+    qw[1::2] *= -1
+    ones_t = torch.ones(T, dtype=torch.float32, device=DEV)
+    ones_n = torch.ones(N, dtype=torch.float32, device=DEV)
+    Y = torch.empty((T, N), dtype=torch.float32, device=DEV)
+    rrs.rrs_gemm(_dev(encode_operand(q, i8)), ones_t, None, _dev(encode_operand(qw, i8)), ones_n, Y, 1.0,
+                 plain=True, i8=i8)
+    torch.cuda.synchronize()
+    exact = q.astype(np.int64) @ qw.astype(np.int64).T
+    assert np.abs(exact).max() > 2 ** 18 and (exact % 2 != 0).any()
+    assert np.array_equal(Y.cpu().numpy().astype(np.int64), exact)
+    assert np.array_equal(Y.cpu().numpy(), exact.astype(np.float32))
+
+
+@pytest.mark.parametrize("L", [256, 512, 1024])
+def test_rrs_gemm_unit_scales_exact_at_large_groups(L):
+    """RRS mode (FP8 carrier) at groups > 128 with s_g = alpha = beta = out_scale = 1: Y = sum_g P_g is an integer
+    below 2^24, so the whole FP32 path (tensor-core group sums + promotion FFMA + epilogue) must return it exactly."""
+    K, T, N = 4096, 130, 240
+    rng = np.random.default_rng(L * 3)
+    q = _adversarial_codes(T, K, L, rng, L != 512)
+    qw = _adversarial_codes(N, K, L, rng, L == 512)
+    qw[::3] *= -1
+    Y = torch.empty((T, N), dtype=torch.float32, device=DEV)
+    rrs.rrs_gemm(_dev(encode_operand(q, False)), torch.ones(T, device=DEV), torch.ones(K // L, device=DEV),
+                 _dev(encode_operand(qw, False)), torch.ones(N, device=DEV), Y, 1.0, group=L)
+    torch.cuda.synchronize()
+    exact = q.astype(np.int64) @ qw.astype(np.int64).T
+    assert np.array_equal(Y.cpu().numpy().astype(np.int64), exact)
+
+
+# --------------------------------------------------------------------------- group-count cap
+
+def test_group_count_cap_refused():
+    """G = K / group > 160 cannot promise the 1e-5 FP32 bound: refused with RRS_ERR_UNSUPPORTED_SHAPE (2) before
+    anything is enqueued; G = 128 at the same K is accepted."""
+    K, T = 8192, 4
+    X = torch.zeros((T, K), dtype=torch.bfloat16, device=DEV)
+    p = torch.arange(K, dtype=torch.int32, device=DEV)
+    xs = torch.empty(T, device=DEV)
+    with pytest.raises(rrs.RRSError) as e:
+        rrs.rrs_rotate_smooth_quant(X, p, None, None, xs, torch.empty(K // 32, device=DEV), group=32)
+    assert e.value.status == 2
+    rrs.rrs_rotate_smooth_quant(X, p, None, torch.empty((T, K), dtype=torch.uint8, device=DEV), xs,
+                                torch.empty(K // 64, device=DEV), group=64)
+    torch.cuda.synchronize()
+
+
+# --------------------------------------------------------------------------- full-size headline, whole rows
+
+def test_full_size_c3_up_full_rows():
+    """bench.py's headline (configs[2] up_proj, 4096 x 4096 x 14336, bf16 Y through rrs_linear) on 48 WHOLE
+    output rows (all 14336 features, 688,128 outputs): every weight row prepared by the oracle, Y within 1 bf16
+    ulp (+ the FP32 allowance) of the oracle's f64 result."""
+    w = WORKLOADS["c3_llama3_8b_up"]
+    X_bits, W_bits, Xc = make_layer(w, index=list(WORKLOADS).index("c3_llama3_8b_up"))
+    perm = _perm(Xc[:256])
+    p = _dev(perm)
+    layer = rrs.RRSLinear(dev_bf16(W_bits), p, keep_packed=True)
+    Y = layer(dev_bf16(X_bits), out_dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    rows = np.sort(np.random.default_rng(3).choice(w.T, size=48, replace=False))
+    Xr = o.rotate(bf16_bits_to_f64(X_bits))
+    s = o.group_scales(o.channel_max(Xr), perm, 128)
+    q, a = o.smooth_quant(Xr[rows], perm, s, 128)
+    qw, beta, _ = o.prepare_weights(bf16_bits_to_f64(W_bits), perm)
+    assert np.array_equal(layer.Wq.cpu().numpy(), o.pack_int4(qw))
+    assert np.array_equal(layer.w_scale.cpu().numpy().view(np.uint32), beta.view(np.uint32))
+    P = o.group_partials(q, qw, 128)
+    Yref = o.scale_accumulate(P, s, a, beta, 1.0 / w.K)
+    ref = dict(P=P, s_group=s, alpha=a, beta=beta, out_scale=1.0 / w.K, Y=Yref)
+    assert bf16_ulp_error(Y.float().cpu().numpy()[rows], Yref, ref) <= 1.0
