@@ -65,6 +65,14 @@ typedef enum { RRS_BF16 = 0, RRS_F32 = 1 } rrs_dtype;
 #define RRS_GEMM_SWIGLU 0x8u  /* rrs_gemm / rrs_linear: fused SwiGLU epilogue, see rrs_gemm */
 #define RRS_GEMM_SUBCHANNEL 0x10u /* rrs_gemm: sub-channel A4W4 baseline, see rrs_gemm */
 #define RRS_TOKEN_SHARDED 0x4u /* rrs_linear with comm: token-sharded data parallel, see below */
+#define RRS_NO_ROTATION 0x40u /* plain Runtime Smooth (Eq. 1-3): no Hadamard on X (prologue) nor
+                                 on W (rrs_prepare_weights); rrs_linear then uses out_scale 1 */
+#define RRS_PREROTATED 0x80u  /* X arrives already rotated (QuaRot-style rotation fused upstream): the prologue
+                                 skips a1; W is prepared as usual (rotated); rrs_linear keeps out_scale 1/K */
+#define RRS_NO_SMOOTH 0x100u  /* efficiency baselines only (SURVEY §8(d) O_quarot / O_plain): skip a2-a5, s_g = 1,
+                                 i.e. per-token RTN of X~ (with RRS_NO_ROTATION: of X) */
+#define RRS_W_PACKED4 0x20u   /* decode regime (configs[3], T <= 64): W kept PACKED at 4 bits ("decode4" layout), see
+                                 rrs_prepare_weights / rrs_gemm / rrs_linear */
 
 typedef struct rrs_comm_s* rrs_comm_t;
 
@@ -72,7 +80,7 @@ typedef struct rrs_comm_s* rrs_comm_t;
 const char* rrs_status_str(int status);
 /* Detail of the last error raised on the calling thread ("" if none). */
 const char* rrs_last_error(void);
-/* ABI version (major * 100 + minor). */
+/* ABI version (major * 100 + minor); 101 added RRS_W_PACKED4, 102 RRS_NO_ROTATION / RRS_PREROTATED / RRS_NO_SMOOTH. */
 int rrs_version(void);
 
 /* Workspace bytes needed by rrs_linear / rrs_rotate_smooth_quant for T tokens:
@@ -98,6 +106,12 @@ rrs_status rrs_perm_from_channel_max(const float* chan_max, int64_t K, int32_t* 
  * Outputs (device, caller-owned; Wq and Wop may each be NULL but not both):
  *   Wq  uint8 [N][K/2] packed INT4;  Wop uint8 [N][K] GEMM operand (flags: RRS_OPERAND_I8 or not);
  *   w_scale f32 [N] = beta_n.
+ * flags & RRS_W_PACKED4: Wop is instead the "decode4" packed W read by the decode GEMM, ceil(N/256)*256*K/2 bytes
+ *   (half the HBM bytes of the one-code-per-byte operand; "different batch sizes"): contiguous 16 KiB tiles,
+ *   tile (rb, kb) = rows [256 rb, 256 rb + 256) x K-block [128 kb, 128 kb + 128) at byte (rb * K/128 + kb) * 16384;
+ *   inside a tile row r occupies 64 bytes at r * 64, its 32-code chunk c (codes j0 = 128 kb + 32 c ..) sits at
+ *   r * 64 + 16 * (c ^ ((r >> 1) & 3)), and chunk byte b (0..15) = (q[j0+b] & 0xF) << 4 | (q[j0+16+b] & 0xF)
+ *   (two's-complement nibbles).  Rows >= N are zero codes.
  * Offline helper: it takes a stream-ordered temporary (cudaMallocAsync, <= 256 MiB) for the rotated rows. */
 rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_t K, int32_t group,
                                const int32_t* perm, uint8_t* Wq, uint8_t* Wop, float* w_scale,
@@ -133,6 +147,9 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
  *   weight rows are interleaved gate/up pairs (row 2i = gate_i, row 2i+1 = up_i, N even) and Y receives
  *   bf16 [T][N/2] with Y[t][i] = bf16_rne(silu(y_2i) * y_2i+1), y = the f32 layer output above and
  *   silu(g) = g / (1 + e^-g) in f32 -- the input of the down_proj RRS layer, written once.  bf16 only.
+ * flags & RRS_W_PACKED4 (decode regime, 1 <= T <= 64, group % 128 == 0): Xop is int8 codes [T][K] (the
+ *   RRS_OPERAND_I8 activation carrier) and Wop the decode4-packed W of rrs_prepare_weights(RRS_W_PACKED4);
+ *   same Y (any fixed FP32 order, R15), no PLAIN / SWIGLU / SUBCHANNEL.
  * Xop uint8 [T][K], x_scale f32 [T], s_group f32 [K/group], Wop uint8 [N][K], w_scale f32 [N];
  * Y [T][ldy] in y_dtype (bf16: round-to-nearest-even of the f32 result), ldy >= N, ldy % 8 == 0. */
 rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_group, const uint8_t* Wop,
@@ -141,6 +158,8 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
 
 /* Whole layer = rrs_rotate_smooth_quant (into ws) + rrs_gemm with out_scale = 1/K.
  * comm == NULL: single GPU, Wop/w_scale hold all N rows.
+ * flags & RRS_W_PACKED4 (comm == NULL, 1 <= T <= 64): Wop is the decode4-packed W; the prologue writes int8
+ *   activation codes to ws and the decode GEMM streams the packed W (see rrs_gemm).
  * comm != NULL (column-parallel): Wop/w_scale hold THIS rank's N/world output rows
  *   [rank*N/world, (rank+1)*N/world); X is replicated; every rank runs the identical prologue; Y
  *   receives all N columns through an NCCL all-gather (any world >= 1; ws sized by rrs_workspace_bytes_comm).

@@ -43,7 +43,7 @@ class RRSLinear:
 
     def __init__(self, W: torch.Tensor, perm: torch.Tensor, comm=None, world: int = 1, rank: int = 0,
                  keep_packed: bool = False, i8: bool = False, group: int = GROUP, token_sharded: bool = False,
-                 swiglu: bool = False, stream=None):
+                 swiglu: bool = False, decode: bool = False, stream=None):
         """token_sharded: data parallel over tokens -- every rank keeps all N rows of W, calls
         with its own token slab and gets its own rows of Y; one all-reduce(MAX) of chan_max per call."""
         N, K = W.shape
@@ -61,6 +61,12 @@ class RRSLinear:
         self.Wq = torch.empty((hi - lo, K // 2), dtype=torch.uint8, device=dev) if keep_packed else None
         self.w_scale = torch.empty(hi - lo, dtype=torch.float32, device=dev)
         rrs_prepare_weights(Wl, self.perm, self.Wq, self.Wop, self.w_scale, i8=i8, stream=stream)
+        # decode regime (T <= 64, configs[3]): W also kept packed at 4 bits for the W-stream GEMM (RRS_W_PACKED4)
+        self.Wp4 = None
+        if decode and not swiglu and comm is None and group % 128 == 0:
+            self.Wp4 = torch.empty(((hi - lo + 255) // 256 * 256, K // 2), dtype=torch.uint8, device=dev)
+            rrs_prepare_weights(Wl, self.perm, None, self.Wp4, torch.empty_like(self.w_scale), packed4=True,
+                                stream=stream)
         self._ws = None
 
     def workspace(self, T: int, device) -> torch.Tensor:
@@ -76,6 +82,10 @@ class RRSLinear:
         T = X.shape[0]
         if Y is None:
             Y = torch.empty((T, self.N_total // (2 if self.swiglu else 1)), dtype=out_dtype, device=X.device)
+        if self.Wp4 is not None and 1 <= T <= 64:
+            rrs_linear(X, self.perm, self.Wp4, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
+                       group=self.group, packed4=True, stream=stream)
+            return Y
         rrs_linear(X, self.perm, self.Wop, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
                    comm=self.comm, group=self.group, i8=self.i8, token_sharded=self.token_sharded,
                    swiglu=self.swiglu, stream=stream)

@@ -22,6 +22,10 @@ RRS_OPERAND_I8 = 0x2
 RRS_TOKEN_SHARDED = 0x4
 RRS_GEMM_SWIGLU = 0x8
 RRS_GEMM_SUBCHANNEL = 0x10
+RRS_W_PACKED4 = 0x20
+RRS_NO_ROTATION = 0x40
+RRS_PREROTATED = 0x80
+RRS_NO_SMOOTH = 0x100
 
 _c_i64, _c_i32, _c_u32, _c_p, _c_sz, _c_f = (ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_void_p,
                                              ctypes.c_size_t, ctypes.c_float)
@@ -139,47 +143,61 @@ def _op_flags(i8: bool) -> int:
     return RRS_OPERAND_I8 if i8 else 0
 
 
-def rrs_prepare_weights(W, perm, Wq, Wop, w_scale, group: int = 128, i8: bool = False, stream=None) -> None:
-    """Wop: uint8 [N][K] GEMM operand bytes (E4M3-encoded codes, or int8 codes with i8=True)."""
+def rrs_prepare_weights(W, perm, Wq, Wop, w_scale, group: int = 128, i8: bool = False, packed4: bool = False,
+                        no_rotation: bool = False, stream=None) -> None:
+    """Wop: uint8 [N][K] GEMM operand bytes (E4M3-encoded codes, or int8 codes with i8=True); with packed4=True
+    Wop is the decode4 tiled nibble layout, ceil(N/256)*256 x K/2 bytes (RRS_W_PACKED4)."""
     N, K = W.shape
     _check("rrs_prepare_weights",
            lib().rrs_prepare_weights(_ptr(W), _bf16_code(W), N, K, group, _ptr(perm), _ptr(Wq), _ptr(Wop),
-                                     _ptr(w_scale), _op_flags(i8), _stream(stream)))
+                                     _ptr(w_scale), _op_flags(i8) | (RRS_W_PACKED4 if packed4 else 0)
+                                     | (RRS_NO_ROTATION if no_rotation else 0), _stream(stream)))
+
+
+def _variant_flags(no_rotation: bool, prerotated: bool, no_smooth: bool) -> int:
+    return ((RRS_NO_ROTATION if no_rotation else 0) | (RRS_PREROTATED if prerotated else 0)
+            | (RRS_NO_SMOOTH if no_smooth else 0))
 
 
 def rrs_rotate_smooth_quant(X, perm, Xq, Xop, x_scale, s_group, chan_max=None, ws=None, group: int = 128,
-                            i8: bool = False, stream=None) -> None:
+                            i8: bool = False, no_rotation: bool = False, prerotated: bool = False,
+                            no_smooth: bool = False, stream=None) -> None:
     T, K = X.shape
     if ws is None:  # marshalling convenience: torch owns the scratch (X~ f32 + chan_max), see rrs_workspace_bytes
         ws = torch.empty(rrs_workspace_bytes(T, 1, K, group, 1), dtype=torch.uint8, device=X.device)
     _check("rrs_rotate_smooth_quant",
            lib().rrs_rotate_smooth_quant(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Xq), _ptr(Xop),
                                          _ptr(x_scale), _ptr(s_group), _ptr(chan_max), _ptr(ws),
-                                         0 if ws is None else ws.numel() * ws.element_size(), _op_flags(i8),
+                                         0 if ws is None else ws.numel() * ws.element_size(),
+                                         _op_flags(i8) | _variant_flags(no_rotation, prerotated, no_smooth),
                                          _stream(stream)))
 
 
 def rrs_gemm(Xop, x_scale, s_group, Wop, w_scale, Y, out_scale: float, plain: bool = False, group: int = 128,
-             i8: bool = False, swiglu: bool = False, subchannel: bool = False, stream=None) -> None:
-    """subchannel: x_scale f32 [G][T], w_scale f32 [G][N] (the sub-channel A4W4 baseline), s_group unused."""
+             i8: bool = False, swiglu: bool = False, subchannel: bool = False, packed4: bool = False,
+             stream=None) -> None:
+    """subchannel: x_scale f32 [G][T], w_scale f32 [G][N] (the sub-channel A4W4 baseline), s_group unused.
+    packed4: decode regime -- Xop int8 codes [T][K], Wop decode4-packed (RRS_W_PACKED4; N is then Y's width)."""
     T, K = Xop.shape
-    N = Wop.shape[0]
+    N = Y.shape[1] * (2 if swiglu else 1) if packed4 else Wop.shape[0]
     flags = (RRS_GEMM_PLAIN if plain else 0) | _op_flags(i8) | (RRS_GEMM_SWIGLU if swiglu else 0) \
-        | (RRS_GEMM_SUBCHANNEL if subchannel else 0)
+        | (RRS_GEMM_SUBCHANNEL if subchannel else 0) | (RRS_W_PACKED4 if packed4 else 0)
     _check("rrs_gemm",
            lib().rrs_gemm(_ptr(Xop), _ptr(x_scale), _ptr(s_group), _ptr(Wop), _ptr(w_scale), T, N, K, group,
                           float(out_scale), flags, _ptr(Y, True), _y_code(Y), Y.stride(0), _stream(stream)))
 
 
 def rrs_linear(X, perm, Wop, w_scale, Y, ws, N_total: int | None = None, comm=None, group: int = 128,
-               i8: bool = False, token_sharded: bool = False, swiglu: bool = False, stream=None) -> None:
+               i8: bool = False, token_sharded: bool = False, swiglu: bool = False, packed4: bool = False,
+               no_rotation: bool = False, prerotated: bool = False, no_smooth: bool = False, stream=None) -> None:
     T, K = X.shape
     N_total = (Y.shape[1] * (2 if swiglu else 1)) if N_total is None else N_total
     _check("rrs_linear",
            lib().rrs_linear(_ptr(X), _bf16_code(X), T, K, group, _ptr(perm), _ptr(Wop), _ptr(w_scale), N_total,
                             _ptr(Y, True), _y_code(Y), Y.stride(0), comm, _ptr(ws), ws.numel() * ws.element_size(),
                             _op_flags(i8) | (RRS_TOKEN_SHARDED if token_sharded else 0)
-                            | (RRS_GEMM_SWIGLU if swiglu else 0), _stream(stream)))
+                            | (RRS_GEMM_SWIGLU if swiglu else 0) | (RRS_W_PACKED4 if packed4 else 0)
+                            | _variant_flags(no_rotation, prerotated, no_smooth), _stream(stream)))
 
 
 def rrs_allgather_columns(Y_shard, Y, comm, ws, stream=None) -> None:

@@ -226,7 +226,7 @@ const char* rrs_status_str(int s) {
 
 const char* rrs_last_error(void) { return g_last_error.c_str(); }
 
-int rrs_version(void) { return 100; }
+int rrs_version(void) { return 102; }
 
 size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world) {
   if (T < 0 || K <= 0 || group <= 0 || K % group || world < 1 || (world > 1 && (N <= 0 || N % world))) return 0;
@@ -260,30 +260,59 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
   if (N < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "N=%lld < 1", (long long)N);
   if (rrs_status s = check_shape(N, K, group)) return s;
   if (!W || !perm || !w_scale || (!Wq && !Wq8)) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+  const bool dec4 = (flags & RRS_W_PACKED4) != 0;  // Wop = decode4-packed [N][K/2] instead of bytes [N][K]
   if (!aligned16(W) || !aligned16(perm) || !aligned16(Wq) || !aligned16(Wq8))
     return fail(RRS_ERR_MISALIGNED, "pointers must be 16-byte aligned");
   // offline path: rotate a chunk of rows into a stream-ordered temporary, then quantise it per row
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(N, (int64_t(256) << 20) / (K * 4)));
   float* tmp = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(float) * chunk * K, st);
+  cudaError_t e = cudaSuccess;
+  if (dec4 && Wq8)  // the decode4 tiles cover ceil(N/256)*256 rows: the padding rows are zero codes
+    e = cudaMemsetAsync(Wop, 0, (size_t)((N + 255) / 256) * 256 * (K / 2), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync (decode4 padding)");
+  e = cudaMallocAsync(reinterpret_cast<void**>(&tmp), sizeof(float) * chunk * K, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync (weight rotation scratch)");
   const uint16_t* Wb = static_cast<const uint16_t*>(W);
   for (int64_t n0 = 0; n0 < N && e == cudaSuccess; n0 += chunk) {
     const int64_t rows = std::min(chunk, N - n0);
-    e = rrs::launch_fwht_colmax(Wb + n0 * K, rows, K, nullptr, tmp, nsm, st);
-    if (e == cudaSuccess)
+    e = (flags & RRS_NO_ROTATION) ? rrs::launch_convert_colmax(Wb + n0 * K, rows, K, nullptr, tmp, nsm, st)
+                                  : rrs::launch_fwht_colmax(Wb + n0 * K, rows, K, nullptr, tmp, nsm, st);
+    if (e == cudaSuccess && (Wq || !dec4))
       e = rrs::launch_smooth_quant(tmp, rows, K, perm, nullptr, nullptr, Wq ? Wq + n0 * (K / 2) : nullptr,
-                                   Wq8 ? Wq8 + n0 * K : nullptr, w_scale + n0, e4m3, 128, nsm, st);
+                                   (Wq8 && !dec4) ? Wq8 + n0 * K : nullptr, w_scale + n0, e4m3, 128, nsm, st);
+    if (e == cudaSuccess && Wq8 && dec4)  // the decode4 packing of the same codes (same kernel, other layout)
+      e = rrs::launch_smooth_quant(tmp, rows, K, perm, nullptr, nullptr, Wop + n0 * (K / 2), nullptr, w_scale + n0,
+                                   e4m3, 128, nsm, st, true);
   }
   cudaError_t e2 = cudaFreeAsync(tmp, st);
   if (e != cudaSuccess) return cuda_fail(e, "weight preparation kernels");
   return e2 == cudaSuccess ? RRS_OK : cuda_fail(e2, "cudaFreeAsync");
 }
 
+// rows a1-a6 (rotate = a1 on, smooth = a2-a5 on; the variants are rrs.h RRS_NO_ROTATION / RRS_PREROTATED and the
+// RRS_NO_SMOOTH efficiency baselines)
 static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* perm, uint8_t* Xq, int8_t* Xq8,
                            float* x_scale, float* s_group, float* chan_max, unsigned* counter, float* Xr, bool e4m3,
-                           int group, int nsm, cudaStream_t st) {
+                           int group, int nsm, cudaStream_t st, bool rotate = true, bool smooth = true) {
+  if (!rotate || !smooth) {  // variant prologue: two kernels
+    cudaError_t e = cudaSuccess;
+    if (smooth) e = cudaMemsetAsync(chan_max, 0, sizeof(float) * K, st);
+    unsigned* cm = smooth ? reinterpret_cast<unsigned*>(chan_max) : nullptr;
+    const uint16_t* Xb = static_cast<const uint16_t*>(X);
+    if (e == cudaSuccess)
+      e = rotate ? rrs::launch_fwht_colmax(Xb, T, K, cm, Xr, nsm, st) : rrs::launch_convert_colmax(Xb, T, K, cm, Xr, nsm, st);
+    if (e == cudaSuccess)
+      e = rrs::launch_smooth_quant(Xr, T, K, perm, cm, s_group, Xq, Xq8, x_scale, e4m3, group, nsm, st);
+    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "variant prologue kernels");
+  }
+  if (T > 0 && rrs::prologue_small_supports(T, K)) {  // decode-sized T: no memset, FWHT over T*K/1024 warps
+    cudaError_t e = rrs::launch_prologue_small(static_cast<const uint16_t*>(X), T, K, Xr, chan_max, nsm, st);
+    if (e == cudaSuccess)
+      e = rrs::launch_smooth_quant(Xr, T, K, perm, reinterpret_cast<const unsigned*>(chan_max), s_group, Xq, Xq8,
+                                   x_scale, e4m3, group, nsm, st);
+    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_small_kernel / smooth_quant_kernel");
+  }
   // chan_max (and the fused kernel's CTA counter) start at zero; one memset when they are contiguous
   const bool contiguous = reinterpret_cast<unsigned*>(chan_max) + K == counter;
   cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * (contiguous ? K + 1 : K), st);
@@ -325,7 +354,8 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
   if (!aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "workspace must be 16-byte aligned");
   if (!chan_max) chan_max = w.chan_max;
   return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, reinterpret_cast<unsigned*>(w.chan_max) + K,
-                  w.Xr, (flags & RRS_OPERAND_I8) == 0, group, nsm, static_cast<cudaStream_t>(stream));
+                  w.Xr, (flags & RRS_OPERAND_I8) == 0, group, nsm, static_cast<cudaStream_t>(stream),
+                  (flags & (RRS_NO_ROTATION | RRS_PREROTATED)) == 0, (flags & RRS_NO_SMOOTH) == 0);
 }
 
 static rrs_status gemm_checks(const int8_t* Xq8, const float* x_scale, const int8_t* Wq8, const float* w_scale,
@@ -353,6 +383,19 @@ rrs_status rrs_gemm(const uint8_t* Xop, const float* x_scale, const float* s_gro
   if (rrs_status s = check_arch(nsm)) return s;
   const bool swiglu = (flags & RRS_GEMM_SWIGLU) != 0;
   if (rrs_status s = gemm_checks(Xq8, x_scale, Wq8, w_scale, T, N, K, group, Y, ldy, swiglu)) return s;
+  if (flags & RRS_W_PACKED4) {
+    if (flags & (RRS_GEMM_PLAIN | RRS_GEMM_SWIGLU | RRS_GEMM_SUBCHANNEL))
+      return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_W_PACKED4: no PLAIN / SWIGLU / SUBCHANNEL");
+    if (!s_group) return fail(RRS_ERR_INVALID_ARGUMENT, "s_group is NULL");
+    if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
+    if (T == 0) return RRS_OK;
+    if (!rrs::decode_gemm_supports(T, K, group))
+      return fail(RRS_ERR_UNSUPPORTED_SHAPE, "RRS_W_PACKED4: 1 <= T <= 64 and group %% 128 == 0 (T=%lld, group=%d)",
+                  (long long)T, group);
+    rrs::DecodeArgs d{Xq8, x_scale, s_group, Wop, w_scale, T, N, K, group, out_scale, Y, y_dtype, ldy};
+    cudaError_t e = rrs::launch_decode_gemm(d, nsm, static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_decode_gemm kernel");
+  }
   const bool plain = (flags & RRS_GEMM_PLAIN) != 0;
   const bool sub = (flags & RRS_GEMM_SUBCHANNEL) != 0;
   if (sub && (plain || swiglu || (flags & RRS_OPERAND_I8) || N % 8 || !aligned16(w_scale)))
@@ -442,6 +485,37 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (rrs_status s = check_shape(T, K, group)) return s;
   const bool swiglu = (flags & RRS_GEMM_SWIGLU) != 0;
   if (swiglu && y_dtype != RRS_BF16) return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_GEMM_SWIGLU: bf16 output only");
+  const bool rotate = (flags & (RRS_NO_ROTATION | RRS_PREROTATED)) == 0, smooth = (flags & RRS_NO_SMOOTH) == 0;
+  if ((flags & RRS_NO_ROTATION) && (flags & RRS_PREROTATED))
+    return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_NO_ROTATION and RRS_PREROTATED are exclusive");
+  if ((!rotate || !smooth) && comm && (flags & RRS_TOKEN_SHARDED))
+    return fail(RRS_ERR_INVALID_ARGUMENT, "prologue variants are not supported with RRS_TOKEN_SHARDED");
+  // R1: (1/sqrt K)^2 when the Hadamard rotation is in the layer (online or pre-applied), exact for K = 2^m
+  const float out_scale = (flags & RRS_NO_ROTATION) ? 1.0f : 1.0f / (float)K;
+  if (flags & RRS_W_PACKED4) {  // decode regime: int8 activation codes + the packed-W stream (decode.cu)
+    if (comm || swiglu) return fail(RRS_ERR_INVALID_ARGUMENT, "RRS_W_PACKED4: single GPU, no SWIGLU");
+    if (T > 0 && !rrs::decode_gemm_supports(T, K, group))
+      return fail(RRS_ERR_UNSUPPORTED_SHAPE, "RRS_W_PACKED4: 1 <= T <= 64 and group %% 128 == 0 (T=%lld, group=%d)",
+                  (long long)T, group);
+    if (N_total < 1) return fail(RRS_ERR_INVALID_ARGUMENT, "N_total=%lld < 1", (long long)N_total);
+    if ((T > 0 && !X) || !perm) return fail(RRS_ERR_INVALID_ARGUMENT, "null pointer");
+    if (y_dtype != RRS_BF16 && y_dtype != RRS_F32) return fail(RRS_ERR_INVALID_ARGUMENT, "y_dtype");
+    Workspace w;
+    const size_t need = carve(ws, T, N_total, K, group, 0, &w);
+    if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
+    if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
+    if (T > 0)
+      if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy)) return s;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max,
+                                reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, /*e4m3=*/false, group, nsm, st,
+                                rotate, smooth))
+      return s;
+    if (T == 0) return RRS_OK;
+    rrs::DecodeArgs d{w.Xq8, w.x_scale, w.s_group, Wop, w_scale, T, N_total, K, group, out_scale, Y, y_dtype, ldy};
+    cudaError_t e = rrs::launch_decode_gemm(d, nsm, st);
+    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "rrs_decode_gemm kernel");
+  }
   if (comm && (flags & RRS_TOKEN_SHARDED))
     return linear_token_sharded(X, T, K, group, perm, Wq8, w_scale, N_total, Y, y_dtype, ldy, comm, ws, ws_bytes, e4m3,
                                 swiglu, nsm, static_cast<cudaStream_t>(stream));
@@ -456,7 +530,6 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(X) || !aligned16(perm) || !aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "16-byte alignment");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const float out_scale = 1.0f / (float)K;  // R1: (1/sqrt K)^2, exact for K = 2^m
   const int esz = y_dtype == RRS_F32 ? 4 : 2;
   // with the fused SwiGLU each rank's shard holds whole (gate, up) pairs and yields n_local / 2 outputs
   const int64_t n_out_local = swiglu ? n_local / 2 : n_local, n_out = swiglu ? N_total / 2 : N_total;
@@ -473,7 +546,7 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
     }
   }
   if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max,
-                              reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, e4m3, group, nsm, st))
+                              reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, e4m3, group, nsm, st, rotate, smooth))
     return s;
   if (T == 0) return RRS_OK;
   if (!comm) {

@@ -50,10 +50,20 @@ bool prologue_fused_supports_k(int64_t K);
 cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
                                   unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,
                                   float* scale, bool e4m3, int group, int nsm, cudaStream_t st);
-// chan_max_bits == nullptr: weight mode (no smoothing, s_group unused)
+// Decode-sized T (1..64, K = 2^m in [1024, 16384]): FWHT spread over T * K/1024 warps, X~ and chan_max written
+// (no memset needed); follow with launch_smooth_quant.
+bool prologue_small_supports(int64_t T, int64_t K);
+cudaError_t launch_prologue_small(const uint16_t* X, int64_t T, int64_t K, float* Xr, float* chan_max, int nsm,
+                                  cudaStream_t st);
+// X~ = X (bf16 -> f32, no rotation) and, unless chan_max_bits is null, the runtime channel max (atomicMax on
+// zeroed float bits) -- the RRS_NO_ROTATION / RRS_PREROTATED prologue and the NO_ROTATION weight path
+cudaError_t launch_convert_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr, int nsm,
+                                  cudaStream_t st);
+// chan_max_bits == nullptr: weight mode (no smoothing, s_group unused).  dec4: Xq in the decode4 nibble layout
+// (rrs.h RRS_W_PACKED4) instead of D4.
 cudaError_t launch_smooth_quant(const float* Xr, int64_t T, int64_t K, const int32_t* perm,
                                 const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                float* scale, bool e4m3, int group, int nsm, cudaStream_t st);
+                                float* scale, bool e4m3, int group, int nsm, cudaStream_t st, bool dec4 = false);
 cudaError_t launch_perm_rank(const float* c, int64_t K, int32_t* perm, cudaStream_t st);
 
 struct GemmArgs {
@@ -79,6 +89,23 @@ struct GemmArgs {
 cudaError_t launch_reduce_splits(const float* part, int splits, int64_t T, int64_t N, void* Y, int y_dtype,
                                  int64_t ldy, cudaStream_t st);
 cudaError_t launch_gemm(const GemmArgs& a, int nsm, cudaStream_t st);
+
+// Decode-regime GEMM (decode.cu): int8 X codes [T][K] x decode4-packed W [N][K/2], T <= 64, group % 128 == 0
+struct DecodeArgs {
+  const int8_t* Xq8;
+  const float* x_scale;
+  const float* s_group;
+  const uint8_t* Wp4;
+  const float* w_scale;
+  int64_t T, N, K;
+  int group;
+  float out_scale;
+  void* Y;
+  int y_dtype;  // 0 = bf16, 1 = f32
+  int64_t ldy;
+};
+bool decode_gemm_supports(int64_t T, int64_t K, int group);
+cudaError_t launch_decode_gemm(const DecodeArgs& a, int nsm, cudaStream_t st);
 
 cudaError_t launch_relayout_shards(const void* src, void* dst, int64_t T, int64_t n_shard, int world,
                                    int64_t ldy, int elem_bytes, cudaStream_t st);

@@ -11,6 +11,7 @@
 //                         (W is permuted, never scaled).
 //   perm_rank_kernel    : offline reorder helper (R5): perm = argsort(c) descending, ties ascending.
 #include <algorithm>
+#include <atomic>
 
 #include "fwht.cuh"
 #include "kernels.h"
@@ -218,7 +219,7 @@ RRS_DEVICE float group_inv_scale(const float* cms, const int (&pj)[32], int j0, 
 template <int TPR, class F>
 RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, bool smooth, float* red, int tid, int rr,
                           int64_t trow, int64_t T, int K, int j0, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
-                          float* __restrict__ scale_out, bool e4m3, F after_reads) {
+                          float* __restrict__ scale_out, bool e4m3, F after_reads, bool dec4 = false) {
   float z[32];
   float m = 0.0f;
 #pragma unroll
@@ -270,15 +271,29 @@ RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, boo
   } else {
     uint32_t packed[4] = {0u, 0u, 0u, 0u};
     uint32_t wide[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    int qv[32];
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
       int q = __float2int_rn(__fmul_rn(z[k], r));  // R10: round half to even
       q = max(-8, min(7, q));                      // R11
-      packed[k >> 3] |= (uint32_t)(q & 0xF) << ((k & 7) * 4);
+      qv[k] = q;
       wide[k >> 2] |= operand_byte(q, e4m3) << ((k & 3) * 8);
     }
     if (Xq) {
-      *reinterpret_cast<uint4*>(Xq + trow * (K / 2) + j0 / 2) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+      int64_t off = trow * (K / 2) + j0 / 2;  // D4: row-major [rows][K/2]
+      if (dec4) {
+        // decode4 layout (rrs.h RRS_W_PACKED4): byte b of the 32-code chunk = q[b] << 4 | q[b + 16] & 0xF; the chunk
+        // sits in the contiguous 16 KiB tile (row block of 256, K-block of 128) at row r, slot c ^ ((r >> 1) & 3)
+#pragma unroll
+        for (int b = 0; b < 16; ++b)
+          packed[b >> 2] |= ((uint32_t)((qv[b] & 0xF) << 4) | (uint32_t)(qv[b + 16] & 0xF)) << ((b & 3) * 8);
+        const int r = (int)(trow & 255), c = (j0 >> 5) & 3;
+        off = (((trow >> 8) * (K >> 7) + (j0 >> 7)) << 14) + r * 64 + ((c ^ ((r >> 1) & 3)) << 4);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) packed[k >> 3] |= (uint32_t)(qv[k] & 0xF) << ((k & 7) * 4);  // D4
+      }
+      *reinterpret_cast<uint4*>(Xq + off) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
     }
     if (Xq8) {
       uint4* dst = reinterpret_cast<uint4*>(Xq8 + trow * K + j0);
@@ -320,10 +335,9 @@ prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __res
     atomicAdd(counter, 1u);
     const unsigned nclusters = gridDim.x / colmax_cluster<K>();
     unsigned v;
-    for (;;) {
+    for (;;) {  // plain spin (one thread per cluster): __nanosleep here cost ~2 us of wake-up latency (trace r2c)
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
       if (v >= nclusters) break;
-      __nanosleep(64);
     }
   }
   ptx::cluster_sync();
@@ -370,6 +384,164 @@ prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __res
   ptx::pdl_launch_dependents();
 }
 
+// ------------------------------------------------------------------------------ a1 + a2, decode-sized T
+//
+// Small-T prologue (T <= 64, K = C * 1024, the decode regime of configs[3]): latency, not throughput, decides, so
+// the FWHT of every row is spread over C independent warps.  H_K = H_C (x) H_1024 (index i = 1024 a + b), and the
+// butterfly stages commute, so warp (t, c) computes output chunk c of row t on its own:
+//   v[b] = sum_a (-1)^popcount(a & c) x[t][1024 a + b]       (the H_C mix, read straight from global memory)
+//   y[1024 c + .] = FWHT_1024(v)                              (5 bits in registers, one warp-private transpose,
+//                                                              5 bits in registers)
+// Every intermediate is a signed subset sum of the row's inputs, so it is exact in fp64 under R3 and the single
+// rounding to f32 gives the correctly rounded X~ (bit-identical to fwht_colmax_kernel).  X~ goes to the workspace;
+// after one grid barrier (cooperative launch; counters in library-owned memory, self-cleaning, so no memset) the
+// grid reduces c_j = max_t |X~_tj| column by column (no atomics).  The quantisation pass is smooth_quant_kernel,
+// chained with programmatic dependent launch.
+__device__ unsigned g_small_bar[256][2];  // [slot][arrive, depart]: zero at module load, reset by the last departer
+
+RRS_DEVICE void grid_barrier_selfclean(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&bar[0], 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < nblocks);
+    if (atomicAdd(&bar[1], 1u) == nblocks - 1) {  // every block has left the spin: reset for the next use
+      bar[0] = 0u;
+      bar[1] = 0u;
+    }
+  }
+  __syncthreads();
+}
+
+template <int C>
+__global__ void __launch_bounds__(128)
+prologue_small_kernel(const uint16_t* __restrict__ X, int T, float* __restrict__ Xr, float* __restrict__ chan_max,
+                      unsigned* __restrict__ bar) {
+  constexpr int K = C * 1024;
+  __shared__ double tr[4][32 * 33];  // warp-private 32 x 32 transpose (row stride 33)
+  ptx::pdl_launch_dependents();      // the quantisation kernel may get resident now (it waits for our completion)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (u < T * C) {
+    const int t = u / C, c = u % C;
+    const uint16_t* row = X + (int64_t)t * K + lane * 32;
+    double v[32];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) v[e] = 0.0;
+#pragma unroll
+    for (int a = 0; a < C; ++a) {
+      const bool neg = __popc(a & c) & 1;
+      const uint4* src = reinterpret_cast<const uint4*>(row + a * 1024);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 w = __ldg(src + q);
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          const double lo = (double)__uint_as_float(ws[h] << 16), hi = (double)__uint_as_float(ws[h] & 0xFFFF0000u);
+          v[q * 8 + 2 * h] = neg ? v[q * 8 + 2 * h] - lo : v[q * 8 + 2 * h] + lo;
+          v[q * 8 + 2 * h + 1] = neg ? v[q * 8 + 2 * h + 1] - hi : v[q * 8 + 2 * h + 1] + hi;
+        }
+      }
+    }
+    butterflies<5>(v);  // bits 0..4 of the chunk position (= e)
+    double* S = tr[warp];
+#pragma unroll
+    for (int e = 0; e < 32; ++e) S[e * 33 + lane] = v[e];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = S[lane * 33 + j];  // now position 32 j + lane
+    butterflies<5>(v);  // bits 5..9
+    float* out = Xr + (int64_t)t * K + c * 1024 + lane;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[32 * j] = __double2float_rn(v[j]);
+  }
+  __threadfence();
+  grid_barrier_selfclean(bar, gridDim.x);
+  // c_j = max_t |X~_tj| (Eq. 1, over all T tokens of the call, R6), one column per thread
+  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < K; col += gridDim.x * blockDim.x) {
+    float m = 0.0f;
+    for (int t = 0; t < T; ++t) m = fmaxf(m, fabsf(__ldcg(Xr + (int64_t)t * K + col)));
+    chan_max[col] = m;
+  }
+}
+
+template <int C>
+static cudaError_t launch_small_k(const uint16_t* X, int64_t T, float* Xr, float* chan_max, unsigned slot, int nsm,
+                                  cudaStream_t st) {
+  auto kern = prologue_small_kernel<C>;
+  const int64_t units = T * C;
+  // one warp per unit; pack up to 4 warps per CTA only when there are more units than SMs
+  const int warps = units >= 4LL * nsm ? 4 : units >= 2LL * nsm ? 2 : 1;
+  const int grid = (int)((units + warps - 1) / warps);
+  void* bar = nullptr;
+  cudaError_t e = cudaGetSymbolAddress(&bar, g_small_bar);
+  if (e != cudaSuccess) return e;
+  unsigned* b = static_cast<unsigned*>(bar) + 2 * (slot & 255u);
+  int Ti = (int)T;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(32 * warps);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, X, Ti, Xr, chan_max, b);
+}
+
+bool prologue_small_supports(int64_t T, int64_t K) {
+  return T >= 1 && T <= 64 && K >= 1024 && K <= 16384 && (K & (K - 1)) == 0;
+}
+
+cudaError_t launch_prologue_small(const uint16_t* X, int64_t T, int64_t K, float* Xr, float* chan_max, int nsm,
+                                  cudaStream_t st) {
+  static std::atomic<unsigned> calls{0};  // barrier slot per call: concurrent calls use different counters
+  const unsigned slot = calls.fetch_add(1u, std::memory_order_relaxed);
+  switch (K) {
+    case 1024: return launch_small_k<1>(X, T, Xr, chan_max, slot, nsm, st);
+    case 2048: return launch_small_k<2>(X, T, Xr, chan_max, slot, nsm, st);
+    case 4096: return launch_small_k<4>(X, T, Xr, chan_max, slot, nsm, st);
+    case 8192: return launch_small_k<8>(X, T, Xr, chan_max, slot, nsm, st);
+    case 16384: return launch_small_k<16>(X, T, Xr, chan_max, slot, nsm, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// ------------------------------------------------------------------------------ a2 without a1 (variants)
+// RRS_NO_ROTATION / RRS_PREROTATED (rrs.h): X~ = X exactly (bf16 -> f32), plus the runtime channel max when
+// chan_max_bits != nullptr (Eq. 1): column j of a row slab per thread, one atomicMax per column per CTA.
+__global__ void __launch_bounds__(256)
+convert_colmax_kernel(const uint16_t* __restrict__ X, int64_t T, int K, int64_t rows_per, float* __restrict__ Xr,
+                      unsigned* __restrict__ chan_max_bits) {
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= K) return;
+  const int64_t t0 = blockIdx.y * rows_per, t1 = t0 + rows_per < T ? t0 + rows_per : T;
+  float m = 0.0f;
+  for (int64_t t = t0; t < t1; ++t) {
+    const float x = __uint_as_float((uint32_t)__ldg(X + t * K + j) << 16);
+    Xr[t * K + j] = x;
+    m = fmaxf(m, fabsf(x));
+  }
+  if (chan_max_bits && t1 > t0) atomicMax(chan_max_bits + j, __float_as_uint(m));
+}
+
+cudaError_t launch_convert_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr, int nsm,
+                                  cudaStream_t st) {
+  if (T <= 0) return cudaSuccess;
+  const int cols = (int)((K + 255) / 256);
+  const int64_t slabs = std::max<int64_t>(1, std::min<int64_t>(T, (4LL * nsm + cols - 1) / cols));
+  const int64_t rows_per = (T + slabs - 1) / slabs;
+  convert_colmax_kernel<<<dim3(cols, (unsigned)((T + rows_per - 1) / rows_per)), 256, 0, st>>>(X, T, (int)K, rows_per,
+                                                                                               Xr, chan_max_bits);
+  return cudaGetLastError();
+}
+
 template <int K>
 struct QuantPlan {
   static constexpr int TPR = K / 32;                                       // threads per row, 32 codes each
@@ -389,7 +561,7 @@ __global__ void __launch_bounds__(QuantPlan<K>::THREADS)
 smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __restrict__ perm,
                     const unsigned* __restrict__ chan_max_bits, float* __restrict__ s_group_out,
                     uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out, int e4m3,
-                    int group) {
+                    int group, int dec4) {
   using Q = QuantPlan<K>;
   constexpr int TPR = Q::TPR;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -418,7 +590,8 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
   trace(1, 0);
   int pj[32];  // perm is an offline input: read it before waiting for the FWHT pass
   load_perm32(perm, j0, pj);
-  ptx::pdl_wait();  // X~ and chan_max come from fwht_colmax_kernel
+  ptx::pdl_launch_dependents();  // the GEMM may get resident (and start its W stream) on SMs we leave free
+  ptx::pdl_wait();  // X~ and chan_max come from fwht_colmax_kernel / prologue_small_kernel
   __syncthreads();
   trace(1, 1);
   if (tid == 0) {  // start the row loads first; the s_g setup below overlaps them
@@ -431,6 +604,8 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
       *reinterpret_cast<uint4*>(cms + c) = __ldcg(reinterpret_cast<const uint4*>(chan_max_bits + c));
     __syncthreads();
     inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out, group);
+  } else if (s_group_out && blockIdx.x == 0) {
+    for (int g = tid; g < K / group; g += Q::THREADS) s_group_out[g] = 1.0f;  // RRS_NO_SMOOTH baseline: s_g = 1
   }
   trace(1, 2);
 
@@ -443,7 +618,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
                    Xq8, scale_out, e4m3 != 0, [&] {
                      if (tid == 0 && tile + STAGES * (int64_t)gridDim.x < ntiles)
                        issue(tile + STAGES * (int64_t)gridDim.x, buf);
-                   });
+                   }, dec4 != 0);
   }
   trace(1, 15);
   ptx::pdl_launch_dependents();
@@ -527,7 +702,7 @@ static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, fl
 template <int K>
 static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* perm, const unsigned* cm,
                                   float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int group, int nsm,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, bool dec4) {
   using Q = QuantPlan<K>;
   auto kern = smooth_quant_kernel<K>;
   cudaError_t e = prepare_kernel(kern, Q::BYTES, Q::THREADS);
@@ -538,7 +713,8 @@ static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* per
     if (cm == nullptr || s_group == nullptr) return cudaSuccess;
     grid = 1;  // T == 0: still publish s_group (all ones, R8)
   }
-  return launch_pdl(kern, grid, Q::THREADS, Q::BYTES, st, Xr, T, perm, cm, s_group, Xq, Xq8, scale, (int)e4m3, group);
+  return launch_pdl(kern, grid, Q::THREADS, Q::BYTES, st, Xr, T, perm, cm, s_group, Xq, Xq8, scale, (int)e4m3, group,
+                    (int)dec4);
 }
 
 #define RRS_FOR_EACH_K(M) M(128) M(256) M(512) M(1024) M(2048) M(4096) M(8192) M(16384) M(7168) M(14336)
@@ -579,9 +755,9 @@ cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned
 
 cudaError_t launch_smooth_quant(const float* Xr, int64_t T, int64_t K, const int32_t* perm,
                                 const unsigned* chan_max_bits, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                float* scale, bool e4m3, int group, int nsm, cudaStream_t st) {
+                                float* scale, bool e4m3, int group, int nsm, cudaStream_t st, bool dec4) {
   switch (K) {
-#define RRS_CASE(k) case k: return launch_quant_k<k>(Xr, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, e4m3, group, nsm, st);
+#define RRS_CASE(k) case k: return launch_quant_k<k>(Xr, T, perm, chan_max_bits, s_group, Xq, Xq8, scale, e4m3, group, nsm, st, dec4);
     RRS_FOR_EACH_K(RRS_CASE)
 #undef RRS_CASE
     default: return cudaErrorInvalidValue;

@@ -66,6 +66,17 @@ RRS_DEV uint32_t ld_dsmem_u32(const void* p, uint32_t rank) {
   asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
   return v;
 }
+RRS_DEV float ld_dsmem_f32(const void* p, uint32_t rank) { return __uint_as_float(ld_dsmem_u32(p, rank)); }
+// 32-bit store into the shared memory of CTA `rank` of this cluster at the address of local `p` (weak; made
+// visible to that CTA by a following cluster barrier)
+RRS_DEV void st_dsmem_f32(void* p, uint32_t rank, float v) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+}
+// the two halves of cluster_sync (arrive with release / wait with acquire), for warps that do work in between
+RRS_DEV void cluster_sync_warps_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+RRS_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 // programmatic dependent launch: wait for the preceding grid's memory; allow the next grid to launch
 RRS_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 RRS_DEV void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
@@ -242,6 +253,15 @@ RRS_DEV void mma_i8(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t 
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// D[tmem] (+)= A[tmem] . B[smem]^T, int8 x int8 -> int32 (A read from tensor memory: M lanes, 4 codes per
+// 32-bit column), issued by one thread
+RRS_DEV void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
 // arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete
 RRS_DEV void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -294,6 +314,16 @@ RRS_DEV void mma_commit(uint64_t* bar) {
 #define RRS_TMEM_ST8(taddr, v)                                                                           \
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),        \
                "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])        \
+               : "memory")
+
+// 32 lanes x 32 columns of 32-bit from 32 registers (v[j] -> column j of the thread's lane)
+#define RRS_TMEM_ST32(taddr, v)                                                                          \
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16," \
+               "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),              \
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),        \
+               "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),  \
+               "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),\
+               "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])\
                : "memory")
 
 RRS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }

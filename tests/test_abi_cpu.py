@@ -49,7 +49,7 @@ def test_binding_names_match_header(lib_path):
 def test_host_only_calls_work_without_gpu(lib_path):
     import paper_2409_20361_b200 as rrs
     l = rrs.lib()
-    assert rrs.rrs_version() == 100
+    assert rrs.rrs_version() == 102
     assert l.rrs_status_str(2) == b"RRS_ERR_UNSUPPORTED_SHAPE"
     # workspace sizing: X~ f32 + chan_max + s_group + x_scale + Xq8, 256-byte aligned
     ws = rrs.rrs_workspace_bytes(2048, 4096, 4096, 128, 1)
@@ -82,7 +82,8 @@ def test_flag_constants_match_header():
     from paper_2409_20361_b200 import _lib
     hdr = open(os.path.join(ROOT, "include", "rrs.h")).read()
     defs = {m.group(1): int(m.group(2), 16) for m in re.finditer(r"#define (RRS_[A-Z0-9_]+) (0x[0-9a-fA-F]+)u", hdr)}
-    assert {"RRS_GEMM_PLAIN", "RRS_OPERAND_I8", "RRS_TOKEN_SHARDED", "RRS_GEMM_SWIGLU", "RRS_GEMM_SUBCHANNEL"} <= set(defs)
+    assert {"RRS_GEMM_PLAIN", "RRS_OPERAND_I8", "RRS_TOKEN_SHARDED", "RRS_GEMM_SWIGLU", "RRS_GEMM_SUBCHANNEL",
+            "RRS_W_PACKED4"} <= set(defs)
     for name, val in defs.items():
         assert getattr(_lib, name) == val, name
     assert len(set(defs.values())) == len(defs)  # distinct bits

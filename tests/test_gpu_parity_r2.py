@@ -91,7 +91,7 @@ def test_group_partials_adversarial_large_groups(L, K, i8):
     rrs.rrs_debug_group_partials(_dev(encode_operand(q, i8)), _dev(encode_operand(qw, i8)), P, group=L, i8=i8)
     torch.cuda.synchronize()
     ref = o.group_partials(q, qw, L)
-    assert np.abs(ref).max() > 2 ** 14
+    assert np.abs(ref).max() >= 49 * (L // 2)  # the designed magnitude (> 2^13 for L >= 512, > 2^14 at 1024)
     assert (ref % 2 != 0).any()
     assert np.array_equal(P.cpu().numpy(), ref)
 

@@ -163,3 +163,26 @@ def test_hadamard_28672_orthogonal_sampled_columns():
             if j0 <= c < j0 + 2048:
                 expect[c - j0, i] = K
         assert np.array_equal(G, expect), j0
+
+
+# -------------------------------------------------------------------------------- Table 4 trend (sanity)
+
+def test_table4_group_size_trend_oracle():
+    """Synthetic Table 4: with the paper's group sizes 1, 32, ..., 512 on channel-outlier activations
+    (the up/gate input profile), plain Runtime Smooth's error grows with the group size while Rotated Runtime
+    Smooth stays flat ("robust to the coarse group scheme").  Method sanity on the oracle, not parity."""
+    from rrs_synth import bf16_bits_to_f64, make_activations, make_weights
+    K, T, N = 1024, 256, 256
+    X = bf16_bits_to_f64(make_activations("channel", T, K, 5, 6))
+    W = bf16_bits_to_f64(make_weights(N, K, 7))
+    Xc = bf16_bits_to_f64(make_activations("channel", 128, K, 5, 8))
+    ref = X @ W.T
+    e_rs, e_rrs = [], []
+    for L in (1, 32, 64, 128, 256, 512):
+        for rot, errs in ((False, e_rs), (True, e_rrs)):
+            Y = o.rrs_linear(X, W, o.calibrate_perm(Xc, rotate_x=rot), L=L, rotate_x=rot, keep_partials=False)["Y"]
+            errs.append(np.linalg.norm(Y - ref) / np.linalg.norm(ref))
+    assert all(b >= a * 0.99 for a, b in zip(e_rs, e_rs[1:])), e_rs
+    assert e_rs[-1] > 1.5 * e_rs[1], e_rs
+    assert max(e_rrs) < 1.15 * min(e_rrs), e_rrs
+    assert e_rrs[-1] < e_rs[-1]
