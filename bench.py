@@ -111,8 +111,13 @@ def max_over_ranks(vals, device, world: int) -> float:
     return float(v.item())
 
 
-def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
-    """Time one workload on this rank; returns the rank-0 summary (other ranks: None)."""
+def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool, i8: bool = False):
+    """Time one workload on this rank; returns the rank-0 summary (other ranks: None).
+
+    Prefill shapes run rrs_linear (fused prologue + tcgen05 pair GEMM).  Decode-sized T (<= 64, configs[3]) runs the
+    decode regime: the small-T prologue (int8 activation codes) + the packed-4-bit W stream GEMM (RRS_W_PACKED4).
+    i8: the int8 operand carrier (tcgen05 kind::i8, int32 group sums -- the north_star's contract path) instead of
+    the default E4M3 carrier (kind::f8f6f4, exact f32 group sums)."""
     import torch
     import torch.distributed as dist
 
@@ -122,6 +127,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
     T, K, N = w.T, w.K, w.N
     out_dtype = torch.bfloat16 if args.out_dtype == "bf16" else torch.float32
     esz = 2 if args.out_dtype == "bf16" else 4
+    decode = T <= 64 and world == 1
 
     # ---- inputs (seeded, synthetic), resident in HBM before timing
     X_bits, W_bits, Xc_bits = make_layer(w, index=list(WORKLOADS).index(wname))
@@ -135,7 +141,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record()
-    layer = rrs.RRSLinear(W_full, perm, comm=comm, world=world, rank=rank)  # a7, offline
+    layer = rrs.RRSLinear(W_full, perm, comm=comm, world=world, rank=rank, i8=i8, decode=decode)  # a7, offline
     t1.record()
     torch.cuda.synchronize()
     prep_ms = t0.elapsed_time(t1)
@@ -151,6 +157,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
     Y = torch.empty((T, N), dtype=out_dtype, device=dev)
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     out_scale = 1.0 / K
+    op_i8 = i8 or decode  # the decode GEMM takes int8 activation codes
 
     def new_events(n, k):
         return [[torch.cuda.Event(enable_timing=True) for _ in range(k)] for _ in range(n)]
@@ -160,8 +167,11 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def linear():  # one whole hot-path step through the public C-ABI entry point (a1-a9, + e when world > 1)
-        rrs.rrs_linear(X, perm, layer.Wop, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
+    def linear(Xin=X):  # one whole hot-path step through the public C-ABI entry point (a1-a9, + e when world > 1)
+        if decode:
+            rrs.rrs_linear(Xin, perm, layer.Wp4, layer.w_scale, Y, ws, N_total=N, packed4=True, stream=stream)
+        else:
+            rrs.rrs_linear(Xin, perm, layer.Wop, layer.w_scale, Y, ws, N_total=N, comm=comm, i8=i8, stream=stream)
 
     # ---- headline: K timed steps of rrs_linear on HBM-resident inputs, L2 flushed before each step
     for _ in range(args.warmup):
@@ -181,43 +191,52 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         wall = time.perf_counter() - wall0
     per_step = [e[0].elapsed_time(e[1]) for e in evs]
 
-    # ---- breakdown (separate pass, events between the kernels): prologue / GEMM / all-gather / plain GEMM
-    # (+ the sub-channel baseline GEMM: its per-group scales are arbitrary positive numbers -- its speed does
-    # not depend on their values -- so this times the kernel, not a quantisation)
-    sub_ok = n_local % 8 == 0
+    # ---- breakdown (separate pass, L2 flushed before each timed piece, events on the launching stream):
+    #   prologue / GEMM / all-gather of the layer; baselines on the SAME codes: the plain per-channel A4W4 GEMM and
+    #   the sub-channel A4W4 GEMM (P:322's two efficiency baselines; the sub-channel scales are arbitrary positive
+    #   numbers -- its speed does not depend on their values), and the prologues of a QuaRot-style layer (online
+    #   rotation + per-token RTN, RRS_NO_SMOOTH) and of a plain A4W4 layer (per-token RTN only) for O_quarot / O_plain
+    sub_ok = n_local % 8 == 0 and not decode and not i8
     G = K // 128
     sub_xs = torch.rand((G, T), dtype=torch.float32, device=dev) + 0.5
     sub_ws = torch.rand((G, n_local), dtype=torch.float32, device=dev) + 0.5
-    bev = new_events(args.steps, 5)
+    Xop_b, xs_b, sg_b = torch.empty_like(Xop), torch.empty_like(xs), torch.empty_like(sg)
+    pieces = {
+        "prologue": lambda: rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, chan_max=cm, ws=pws, i8=op_i8,
+                                                        stream=stream),
+        "rrs_gemm": (lambda: rrs.rrs_gemm(Xop, xs, sg, layer.Wp4, layer.w_scale, Y_shard, out_scale, packed4=True,
+                                          stream=stream)) if decode else
+                    (lambda: rrs.rrs_gemm(Xop, xs, sg, layer.Wop, layer.w_scale, Y_shard, out_scale, i8=i8,
+                                          stream=stream)),
+        "quarot_prologue": lambda: rrs.rrs_rotate_smooth_quant(X, perm, None, Xop_b, xs_b, sg_b, ws=pws, i8=op_i8,
+                                                               no_smooth=True, stream=stream),
+        "plain_prologue": lambda: rrs.rrs_rotate_smooth_quant(X, perm, None, Xop_b, xs_b, sg_b, ws=pws, i8=op_i8,
+                                                              no_smooth=True, no_rotation=True, stream=stream),
+    }
+    if not decode:
+        pieces["plain_gemm"] = lambda: rrs.rrs_gemm(Xop, xs, None, layer.Wop, layer.w_scale, Y_shard, out_scale,
+                                                    plain=True, i8=i8, stream=stream)
+    if sub_ok:
+        pieces["subchannel_gemm"] = lambda: rrs.rrs_gemm(Xop, sub_xs, None, layer.Wop, sub_ws, Y_shard, out_scale,
+                                                         subchannel=True, stream=stream)
+    if world > 1:
+        pieces["allgather"] = lambda: rrs.rrs_allgather_columns(Y_shard, Y, comm, ws, stream=stream)
+    if decode:  # the round-1 decode path (one byte per W code, split-K GEMM) on the same layer, for comparison
+        pieces["r1_byte_operand_layer"] = lambda: rrs.rrs_linear(X, perm, layer.Wop, layer.w_scale, Y, ws, N_total=N,
+                                                                 stream=stream)
+    times = {k: [] for k in pieces}
+    rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, chan_max=cm, ws=pws, i8=op_i8, stream=stream)
     for i in range(args.warmup + args.steps):
-        ev = bev[i - args.warmup] if i >= args.warmup else new_events(1, 5)[0]
-        flush.zero_()
-        ev[0].record(stream)
-        rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, chan_max=cm, ws=pws, stream=stream)
-        ev[1].record(stream)
-        rrs.rrs_gemm(Xop, xs, sg, layer.Wop, layer.w_scale, Y_shard, out_scale, stream=stream)
-        ev[2].record(stream)
-        if world > 1:
-            rrs.rrs_allgather_columns(Y_shard, Y, comm, ws, stream=stream)
-        ev[3].record(stream)
-        flush.zero_()
-        ev[4].record(stream)  # plain per-channel A4W4 GEMM on the same operands (P:322 baseline)
-        rrs.rrs_gemm(Xop, xs, None, layer.Wop, layer.w_scale, Y_shard, out_scale, plain=True, stream=stream)
-        ev.append(torch.cuda.Event(enable_timing=True))
-        ev[5].record(stream)
-        if sub_ok:  # sub-channel A4W4 GEMM (P:322's second baseline) on the same codes
+        evp = {k: new_events(1, 2)[0] for k in pieces}
+        for k, fn in pieces.items():
             flush.zero_()
-            ev.append(torch.cuda.Event(enable_timing=True))
-            ev.append(torch.cuda.Event(enable_timing=True))
-            ev[6].record(stream)
-            rrs.rrs_gemm(Xop, sub_xs, None, layer.Wop, sub_ws, Y_shard, out_scale, subchannel=True, stream=stream)
-            ev[7].record(stream)
-    torch.cuda.synchronize()
-    prologue = [e[0].elapsed_time(e[1]) for e in bev]
-    gemm = [e[1].elapsed_time(e[2]) for e in bev]
-    gather = [e[2].elapsed_time(e[3]) for e in bev]
-    plain = [e[4].elapsed_time(e[5]) for e in bev]
-    subch = [e[6].elapsed_time(e[7]) for e in bev] if sub_ok else [0.0]
+            evp[k][0].record(stream)
+            fn()
+            evp[k][1].record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            for k in pieces:
+                times[k].append(evp[k][0].elapsed_time(evp[k][1]))
 
     # ---- end to end through the public API with host buffers: pinned H2D of X, rrs_linear, D2H of Y
     X_host = X.cpu().pin_memory()
@@ -229,7 +248,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
         ev = eev[i - args.warmup] if i >= args.warmup else new_events(1, 2)[0]
         ev[0].record(stream)
         X_dev.copy_(X_host, non_blocking=True)
-        rrs.rrs_linear(X_dev, perm, layer.Wop, layer.w_scale, Y, ws, N_total=N, comm=comm, stream=stream)
+        linear(X_dev)
         Y_host.copy_(Y, non_blocking=True)
         ev[1].record(stream)
     torch.cuda.synchronize()
@@ -238,34 +257,42 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool):
     def mx(vals):
         return max_over_ranks(vals, dev, world)
 
-    ms_step, ms_pro, ms_gemm, ms_gather = mx(per_step), mx(prologue), mx(gemm), mx(gather)
-    ms_plain, ms_e2e, ms_sub = mx(plain), mx(e2e), mx(subch)
+    ms_step, ms_e2e = mx(per_step), mx(e2e)
+    bd = {k: mx(v) for k, v in times.items()}
     ck = clocks.summary()
     if world > 1:
         dist.barrier()
     if rank != 0:
         return None
     ops = 2.0 * T * K * N
-    gemm_tops = 2.0 * T * K * n_local / (ms_gemm * 1e-3) / 1e12
+    gemm_tops = 2.0 * T * K * n_local / (bd["rrs_gemm"] * 1e-3) / 1e12
+    bd["prepare_weights_offline"] = prep_ms
     res = {
-        "workload": wname, "T": T, "K": K, "N": N, "ms_per_step": ms_step,
+        "workload": wname, "T": T, "K": K, "N": N, "ms_per_step": ms_step, "carrier": "int8" if op_i8 else "e4m3",
+        "path": "decode (small-T prologue + packed-4-bit W stream GEMM)" if decode else "prefill",
         "tops": ops / (ms_step * 1e-3) / 1e12, "tokens_per_s": T / (ms_step * 1e-3),
-        "breakdown_ms": {"prologue": ms_pro, "rrs_gemm": ms_gemm, "allgather": ms_gather,
-                         "plain_gemm": ms_plain, "subchannel_gemm": ms_sub if sub_ok else None,
-                         "prepare_weights_offline": prep_ms},
-        "gemm_tops": gemm_tops, "rrs_overhead_vs_plain_gemm": ms_gemm / ms_plain - 1.0,
+        "breakdown_ms": bd, "gemm_tops": gemm_tops,
         "e2e_tops": ops / (ms_e2e * 1e-3) / 1e12, "h2d": T * K * 2, "d2h": T * N * esz,
         "clocks": ck, "wall_s_timed_region": wall,
     }
+    if "plain_gemm" in bd:
+        res["rrs_overhead_vs_plain_gemm"] = bd["rrs_gemm"] / bd["plain_gemm"] - 1.0  # O_gemm
+        res["o_quarot"] = ms_step / (bd["quarot_prologue"] + bd["plain_gemm"]) - 1.0
+        res["o_plain"] = ms_step / (bd["plain_prologue"] + bd["plain_gemm"]) - 1.0
+    if decode:
+        wbytes = layer.Wp4.numel()
+        res["w_stream_gbs"] = wbytes / (bd["rrs_gemm"] * 1e-3) / 1e9
+        res["w_bytes"] = wbytes
     if cpu_base:
         res["cpu_baseline"] = cpu_baseline(w, X_bits, W_bits, Xc_bits, budget_s=args.cpu_budget)
     return res
 
 
-def measure_mlp(args, dev):
+def measure_mlp(args, dev, prerotated: bool = False):
     """SURVEY §8 f1 on config C3 (LLaMA-3-8B MLP, 4096-token prefill, D = 4096, F = 14336), single GPU:
     h = SwiGLU fused into ONE RRS GEMM over the interleaved gate/up rows (one prologue on X), then the
-    down_proj RRS layer on h.  Ops = 2 T D (2F) + 2 T F D."""
+    down_proj RRS layer on h.  Ops = 2 T D (2F) + 2 T F D.  prerotated: the up/gate input arrives already rotated
+    (RRS_PREROTATED: its prologue skips the online FWHT; down_proj still rotates online)."""
     import torch
 
     import paper_2409_20361_b200 as rrs
@@ -281,7 +308,7 @@ def measure_mlp(args, dev):
     Wg, Wu_, Wd = (dev_bf16(make_weights(*shape, seed)) for shape, seed in
                    (((F, D), 7101), ((F, D), 7102), ((D, F), 7103)))
     perm_in = rrs.calibrate_perm(Xc)
-    up_gate = rrs.RRSLinear(rrs.interleave_gate_up(Wg, Wu_), perm_in, swiglu=True)
+    up_gate = rrs.RRSLinear(rrs.interleave_gate_up(Wg, Wu_), perm_in, swiglu=True, prerotated=prerotated)
     perm_mid = rrs.calibrate_perm(up_gate(Xc))  # offline reorder of the down_proj input (R5)
     down = rrs.RRSLinear(Wd, perm_mid)
     del Wg, Wu_, Wd
@@ -306,7 +333,8 @@ def measure_mlp(args, dev):
     return {"ms_per_step": step, "tops": ops / (step * 1e-3) / 1e12, "tokens_per_s": T / (step * 1e-3),
             "breakdown_ms": {"up_gate_swiglu (prologue + one GEMM over 2F rows)": ug,
                              "down_proj (K = 14336 prologue + GEMM)": dn},
-            "note": "SURVEY 8 f1: LLaMA-3-8B MLP block, T=4096 D=4096 F=14336, bf16 h and Y, L2 flushed per step"}
+            "note": "SURVEY 8 f1: LLaMA-3-8B MLP block, T=4096 D=4096 F=14336, bf16 h and Y, L2 flushed per step"
+                    + ("; up/gate input pre-rotated (RRS_PREROTATED, P:138)" if prerotated else "")}
 
 
 def run_gpu(args):
@@ -329,15 +357,25 @@ def run_gpu(args):
     head = measure_workload(args, args.workload, dev, world, rank, comm,
                             cpu_base=(world == 1 and not args.no_cpu_baseline))
     extras = {}
+    keep = ("path", "carrier", "ms_per_step", "tops", "tokens_per_s", "breakdown_ms", "gemm_tops",
+            "rrs_overhead_vs_plain_gemm", "o_quarot", "o_plain", "w_stream_gbs", "e2e_tops")
     for wn in (args.also.split(",") if args.also else []):
-        if wn == "c3_llama3_8b_mlp":
+        if wn.startswith("c3_llama3_8b_mlp"):
             if world == 1:
-                extras[wn] = measure_mlp(args, dev)
+                extras[wn] = measure_mlp(args, dev, prerotated=wn.endswith("_prerotated"))
             continue
-        r = measure_workload(args, wn, dev, world, rank, comm, cpu_base=False)
+        i8 = wn.endswith("_i8")
+        r = measure_workload(args, wn[:-3] if i8 else wn, dev, world, rank, comm, cpu_base=False, i8=i8)
         if r is not None:
-            extras[wn] = {k: r[k] for k in ("ms_per_step", "tops", "tokens_per_s", "breakdown_ms", "gemm_tops",
-                                            "rrs_overhead_vs_plain_gemm", "e2e_tops")}
+            extras[wn] = {k: r[k] for k in keep if k in r}
+            if "w_stream_gbs" in r:  # decode: the W stream against the HBM roofline
+                pk = peaks()
+                extras[wn]["roofline"] = {
+                    "bound": "hbm", "kernel": "rrs_decode_gemm_kernel", "achieved": r["w_stream_gbs"],
+                    "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": r["w_stream_gbs"] / pk["hbm_gbs"],
+                    "algorithmic": f"packed 4-bit W ({r['w_bytes']} B) per launch / decode GEMM CUDA-event time",
+                    "step_frac": (r["w_bytes"] / (pk["hbm_gbs"] * 1e9)) / (r["ms_per_step"] * 1e-3),
+                    "step_frac_note": "whole layer step vs its W-stream floor (W bytes / HBM peak)"}
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -347,6 +385,8 @@ def run_gpu(args):
 
     pk = peaks()
     int8_peak = pk["bf16_tflops"] * INT8_OVER_BF16
+    sm_mhz = (head["clocks"] or {}).get("sm_mhz") or 1965.0
+    micro_peak = 8189.0 * 2 * 148 * sm_mhz * 1e6 / 1e12  # tcgen05 microbenchmark: 8189 MAC/clk/SM (profiles/micro_r1.txt)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
@@ -354,6 +394,13 @@ def run_gpu(args):
             traffic = json.load(fh).get(args.workload, {}).get("gemm_dram_bytes_per_launch")
     w = WORKLOADS[args.workload]
     pow2 = (w.K & (w.K - 1)) == 0  # K = 2^m: the single-launch fused prologue
+    # prologue rooflines: FP64 DADDs of the exact FWHT (K log2 K per token; 28*2^m: m + 14 per element)
+    # against 64 DADD/clk/SM, and algorithmic HBM bytes (2K read + K operand bytes + 4 per token, 4K + 4G per call)
+    a_k = (w.K.bit_length() - 1) if pow2 else ((w.K // 28).bit_length() - 1 + 14)
+    t_pro = head["breakdown_ms"]["prologue"] * 1e-3
+    dadd = float(w.T) * w.K * a_k
+    fp64_peak = 64.0 * 148 * sm_mhz * 1e6
+    pro_bytes = w.T * (3.0 * w.K + 4) + 4.0 * w.K + 4.0 * (w.K // 128)
     out = {
         "metric": METRIC,
         "value": head["tops"],
@@ -365,7 +412,7 @@ def run_gpu(args):
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
-        "dtype": "int8",
+        "dtype": "int4 codes (e4m3 carrier: tcgen05 kind::f8f6f4, exact f32 group sums; fp64 rotation, f32 scales)",
         "data": "synthetic (seeded LLaMA-like bf16 activations, N(0,0.02^2) bf16 weights; rrs_synth)",
         "config": {"workload": args.workload, "T": w.T, "K": w.K, "N": w.N, "group": 128,
                    "out_dtype": args.out_dtype, "note": w.note,
@@ -376,12 +423,26 @@ def run_gpu(args):
         "breakdown_ms": head["breakdown_ms"],
         "gemm_tops": head["gemm_tops"],
         "gemm_pct_int8_peak": 100.0 * head["gemm_tops"] / int8_peak,
-        "rrs_overhead_vs_plain_gemm": head["rrs_overhead_vs_plain_gemm"],
+        "rrs_overhead_vs_plain_gemm": head.get("rrs_overhead_vs_plain_gemm"),
+        "o_quarot": head.get("o_quarot"),
+        "o_plain": head.get("o_plain"),
         "roofline": {"bound": "tensor", "kernel": "rrs_gemm_kernel", "achieved": head["gemm_tops"],
                      "peak": int8_peak, "unit": "TFLOP/s", "frac": head["gemm_tops"] / int8_peak,
                      "traffic": traffic,
-                     "peak_src": f"int8 = {INT8_OVER_BF16:g} x bf16 burst {pk['bf16_tflops']} TFLOP/s, {pk['src']}",
+                     "peak_src": f"int8/fp8 = {INT8_OVER_BF16:g} x bf16 burst {pk['bf16_tflops']} TFLOP/s, {pk['src']}",
+                     "frac_vs_tcgen05_microbench": head["gemm_tops"] / micro_peak,
+                     "tcgen05_microbench_peak": micro_peak,
+                     "frac_vs_nominal_4500": head["gemm_tops"] / 4500.0,
                      "algorithmic": "2*T*K*N_local int ops per launch / rrs_gemm CUDA-event time (SURVEY 8(d))"},
+        "prologue_roofline": {"bound": "fp64", "kernel": "prologue_fused_kernel" if pow2 else
+                              "fwht_colmax_kernel + smooth_quant_kernel",
+                              "achieved": dadd / t_pro / 1e12, "peak": fp64_peak / 1e12, "unit": "T DADD/s",
+                              "frac": dadd / t_pro / fp64_peak,
+                              "hbm_achieved_gbs": pro_bytes / t_pro / 1e9, "hbm_peak_gbs": pk["hbm_gbs"],
+                              "hbm_frac": pro_bytes / t_pro / 1e9 / pk["hbm_gbs"],
+                              "algorithmic": f"T*K*{a_k} DADD (exact FWHT) and T*(3K+4)+4K+4G bytes per call"},
+        "headline_context": {k: {kk: extras[k].get(kk) for kk in ("tops", "ms_per_step", "rrs_overhead_vs_plain_gemm")}
+                             for k in ("c3_llama3_8b_down", "c3_llama3_8b_mlp") if k in extras},
         "e2e": {"value": head["e2e_tops"], "unit": "TOPS", "h2d_bytes_per_step": head["h2d"],
                 "d2h_bytes_per_step": head["d2h"],
                 "api": "rrs_linear (pinned host X -> device -> host Y, copies inside the timed region)"},
@@ -486,7 +547,8 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["rrs", "reference"], default="rrs")
     ap.add_argument("--workload", default="c3_llama3_8b_up", choices=sorted(WORKLOADS))
-    ap.add_argument("--also", default="c3_llama3_8b_down,c2_llama2_7b_qo,c3_llama3_8b_mlp,c4_decode_t64,c4_decode_t1",
+    ap.add_argument("--also", default="c3_llama3_8b_down,c3_llama3_8b_mlp,c3_llama3_8b_mlp_prerotated,c3_llama3_8b_up_i8,"
+                                      "c2_llama2_7b_qo,c4_decode_t64,c4_decode_t1,c5_llama3_70b_up_rank8",
                     help="comma-separated extra workloads summarised under 'also' (empty: none)")
     ap.add_argument("--out-dtype", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=20.0)

@@ -26,7 +26,19 @@ int main(int argc, char** argv) {
   cudaMemcpy(perm, hp.data(), K * 4, cudaMemcpyHostToDevice);
   unsigned* counter;
   cudaMalloc(&counter, 256);
-  const bool fused = argc > 3 && atoi(argv[3]) != 0;
+  const bool fused = argc > 3 && atoi(argv[3]) == 1;
+  const bool decode = argc > 3 && atoi(argv[3]) == 2;
+  for (int rep = 0; rep < 3 && decode; ++rep) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    cudaError_t le = rrs::launch_prologue_decode(X, T, K, perm, cm, Xr, sg, nullptr, q, sc, false, 128, 0);
+    cudaEventRecord(e1);
+    cudaError_t e = cudaDeviceSynchronize();
+    float a;
+    cudaEventElapsedTime(&a, e0, e1);
+    printf("rep %d: %s / %s decode prologue %.1f us\n", rep, cudaGetErrorString(le), cudaGetErrorString(e), a * 1e3);
+  }
   for (int rep = 0; rep < 3 && fused; ++rep) {
     cudaMemset(cm, 0, K * 4);
     cudaMemset(counter, 0, 4);
@@ -40,7 +52,7 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&a, e0, e1);
     printf("rep %d: %s fused prologue %.1f us\n", rep, cudaGetErrorString(e), a * 1e3);
   }
-  for (int rep = 0; rep < 3 && !fused; ++rep) {
+  for (int rep = 0; rep < 3 && !fused && !decode; ++rep) {
     cudaMemset(cm, 0, K * 4);
     cudaEvent_t e0, e1, e2;
     cudaEventCreate(&e0); cudaEventCreate(&e1); cudaEventCreate(&e2);
@@ -54,9 +66,9 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&a, e0, e1); cudaEventElapsedTime(&b, e1, e2);
     printf("rep %d: %s fwht_colmax %.1f us, smooth_quant %.1f us\n", rep, cudaGetErrorString(e), a * 1e3, b * 1e3);
   }
-  static unsigned long long h[2][1024][16];
+  static unsigned long long h[3][1024][16];
   cudaMemcpyFromSymbol(h, rrs::g_trace, sizeof(h));
-  for (int k = 0; k < 2; ++k) {
+  for (int k = 0; k < 3; ++k) {
     unsigned long long t0 = ~0ull;
     int n = 0;
     for (int c = 0; c < 1024; ++c) if (h[k][c][0]) { t0 = std::min(t0, h[k][c][0]); n = c + 1; }

@@ -194,6 +194,11 @@ int32_t rrs_comm_rank(rrs_comm_t comm);
 /* Test-only exports (same kernels, extra stores). */
 /* X~ as f32 [T][K] (natural column order) and chan_max f32 [K] from the a1/a2 kernel. */
 rrs_status rrs_debug_rotate(const void* X, int64_t T, int64_t K, float* Xr, float* chan_max, void* stream);
+/* The column-parallel layer's re-layout step on its own (the step after ncclAllGather): gathered =
+ * [world][T][n_shard] (rank-major, as ncclAllGather leaves it) -> Y[T][ldy] with rank r's shard in columns
+ * [r n_shard, (r+1) n_shard).  Lets a single GPU emulate P ranks bit for bit (tests T3a). */
+rrs_status rrs_debug_relayout(const void* gathered, int64_t T, int64_t n_shard, int32_t world, int32_t y_dtype,
+                              void* Y, int64_t ldy, void* stream);
 /* The tcgen05 GEMM's own group partials P[G][T][N] as int32 (read back from TMEM, same kernel). */
 rrs_status rrs_debug_group_partials(const uint8_t* Xop, const uint8_t* Wop, int64_t T, int64_t N, int64_t K,
                                     int32_t group, int32_t* P, uint32_t flags, void* stream);

@@ -11,7 +11,7 @@ from __future__ import annotations
 import torch
 
 from ._lib import (EXPORTS, RRSError, lib, rrs_allgather_columns, rrs_comm_destroy, rrs_comm_init, rrs_comm_unique_id,  # noqa: F401
-                   rrs_debug_group_partials, rrs_debug_rotate, rrs_gemm, rrs_linear, rrs_perm_from_channel_max,
+                   rrs_debug_group_partials, rrs_debug_relayout, rrs_debug_rotate, rrs_gemm, rrs_linear, rrs_perm_from_channel_max,
                    rrs_prepare_weights, rrs_rotate_smooth_quant, rrs_version, rrs_workspace_bytes,
                    rrs_workspace_bytes_comm)
 
@@ -43,7 +43,7 @@ class RRSLinear:
 
     def __init__(self, W: torch.Tensor, perm: torch.Tensor, comm=None, world: int = 1, rank: int = 0,
                  keep_packed: bool = False, i8: bool = False, group: int = GROUP, token_sharded: bool = False,
-                 swiglu: bool = False, decode: bool = False, stream=None):
+                 swiglu: bool = False, decode: bool = False, prerotated: bool = False, stream=None):
         """token_sharded: data parallel over tokens -- every rank keeps all N rows of W, calls
         with its own token slab and gets its own rows of Y; one all-reduce(MAX) of chan_max per call."""
         N, K = W.shape
@@ -52,6 +52,8 @@ class RRSLinear:
         self.comm, self.world, self.rank = comm, world, rank
         self.token_sharded = token_sharded
         self.swiglu = swiglu  # rows are interleaved (gate_i, up_i) pairs; output = silu(gate) * up, N/2 columns
+        # the input arrives already rotated (QuaRot-style rotation fused upstream): skip the online a1
+        self.prerotated = prerotated
         lo, hi = (0, N) if token_sharded else shard_rows(N, world, rank)
         Wl = W[lo:hi].contiguous()
         dev = W.device
@@ -84,11 +86,11 @@ class RRSLinear:
             Y = torch.empty((T, self.N_total // (2 if self.swiglu else 1)), dtype=out_dtype, device=X.device)
         if self.Wp4 is not None and 1 <= T <= 64:
             rrs_linear(X, self.perm, self.Wp4, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
-                       group=self.group, packed4=True, stream=stream)
+                       group=self.group, packed4=True, prerotated=self.prerotated, stream=stream)
             return Y
         rrs_linear(X, self.perm, self.Wop, self.w_scale, Y, self.workspace(T, X.device), N_total=self.N_total,
                    comm=self.comm, group=self.group, i8=self.i8, token_sharded=self.token_sharded,
-                   swiglu=self.swiglu, stream=stream)
+                   swiglu=self.swiglu, prerotated=self.prerotated, stream=stream)
         return Y
 
 
@@ -107,8 +109,12 @@ class RRSMLP:
         Y = RRS(h) W_down^T                 -- the down_proj RRS layer (K = F, e.g. 14336 = 28 * 512)
     perm_in / perm_mid: offline reorders of X and of h (calibrate_perm on calibration activations)."""
 
-    def __init__(self, W_gate, W_up, W_down, perm_in, perm_mid, i8: bool = False, stream=None):
-        self.up_gate = RRSLinear(interleave_gate_up(W_gate, W_up), perm_in, i8=i8, swiglu=True, stream=stream)
+    def __init__(self, W_gate, W_up, W_down, perm_in, perm_mid, i8: bool = False, prerotated_input: bool = False,
+                 stream=None):
+        """prerotated_input: X arrives already rotated (the paper rotates online only before the output and
+        down projectors; the up/gate input carries the rotation fused into the residual stream)."""
+        self.up_gate = RRSLinear(interleave_gate_up(W_gate, W_up), perm_in, i8=i8, swiglu=True,
+                                 prerotated=prerotated_input, stream=stream)
         self.down = RRSLinear(W_down, perm_mid, i8=i8, stream=stream)
 
     def __call__(self, X: torch.Tensor, out_dtype=torch.bfloat16, stream=None):

@@ -53,6 +53,7 @@ _SIGS = {
     "rrs_comm_rank": (_c_i32, [_c_p]),
     "rrs_debug_rotate": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_p, _c_p, _c_p]),
     "rrs_debug_group_partials": (ctypes.c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i64, _c_i32, _c_p, _c_u32, _c_p]),
+    "rrs_debug_relayout": (ctypes.c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_i64, _c_p]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -236,3 +237,11 @@ def rrs_debug_group_partials(Xop, Wop, P, group: int = 128, i8: bool = False, st
     _check("rrs_debug_group_partials",
            lib().rrs_debug_group_partials(_ptr(Xop), _ptr(Wop), T, N, K, group, _ptr(P), _op_flags(i8),
                                           _stream(stream)))
+
+
+def rrs_debug_relayout(gathered, Y, stream=None) -> None:
+    """gathered: [world][T][n_shard] (f32 or bf16) -> Y[T][world * n_shard] (unit column stride, any row stride)."""
+    world, T, ns = gathered.shape
+    _check("rrs_debug_relayout",
+           lib().rrs_debug_relayout(_ptr(gathered), T, ns, world, _y_code(gathered), _ptr(Y, True), Y.stride(0),
+                                    _stream(stream)))

@@ -3,6 +3,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -146,6 +147,7 @@ struct rrs_comm_s {
   cudaEvent_t ev[9] = {};       // [0..7] slab GEMM done, [8] side stream done
 };
 constexpr int kMaxSlabs = 8;
+constexpr int kNcclCtas = 16;  // SMs left to NCCL while a slab GEMM runs
 
 static rrs_status gather_columns(const void* shard, int64_t T, int64_t N_total, int esz, void* Y, int64_t ldy,
                                  rrs_comm_t comm, void* gather_buf, cudaStream_t st) {
@@ -306,12 +308,11 @@ static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* p
       e = rrs::launch_smooth_quant(Xr, T, K, perm, cm, s_group, Xq, Xq8, x_scale, e4m3, group, nsm, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "variant prologue kernels");
   }
-  if (T > 0 && rrs::prologue_small_supports(T, K)) {  // decode-sized T: no memset, FWHT over T*K/1024 warps
-    cudaError_t e = rrs::launch_prologue_small(static_cast<const uint16_t*>(X), T, K, Xr, chan_max, nsm, st);
-    if (e == cudaSuccess)
-      e = rrs::launch_smooth_quant(Xr, T, K, perm, reinterpret_cast<const unsigned*>(chan_max), s_group, Xq, Xq8,
-                                   x_scale, e4m3, group, nsm, st);
-    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_small_kernel / smooth_quant_kernel");
+  if (T > 0 && rrs::prologue_decode_supports(T, K, group)) {  // decode-sized T: one launch, no memset
+    cudaError_t e = rrs::launch_prologue_decode(static_cast<const uint16_t*>(X), T, K, perm,
+                                                reinterpret_cast<unsigned*>(chan_max), Xr, s_group, Xq, Xq8, x_scale,
+                                                e4m3, group, st);
+    return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_decode_kernel");
   }
   // chan_max (and the fused kernel's CTA counter) start at zero; one memset when they are contiguous
   const bool contiguous = reinterpret_cast<unsigned*>(chan_max) + K == counter;
@@ -559,7 +560,12 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
   // Token slabs (SURVEY §8(e) "overlap by token slabs"): the GEMM of slab s runs on `st` while the all-gather
   // and relayout of slab s-1 run on the communicator's side stream, so the NVLink transfer overlaps compute.
   // Slabs are whole 256-row M-blocks of the pair GEMM; the shard / gather buffers are laid out slab-major.
-  const int64_t rows = T >= 1024 ? (((T + 3) / 4 + 255) / 256) * 256 : T;
+  // Slabs only while each slab's GEMM still fills the SMs it may use (pair tiles of 256 x 240 >= the pairs left
+  // after kNcclCtas): at P = 8 on the C3 up shard (1792 columns) a quarter slab would fill only a third of them.
+  const int64_t n_tiles = (n_local + 239) / 240, m_tiles = (T + 255) / 256;
+  const int64_t pairs = (nsm - kNcclCtas) / 2;
+  const int64_t want = std::max<int64_t>(1, std::min<int64_t>(4, (m_tiles * n_tiles) / std::max<int64_t>(1, pairs)));
+  const int64_t rows = want > 1 ? ((m_tiles + want - 1) / want) * 256 : T;
   const int nslab = (int)((T + rows - 1) / rows);
   if (nslab > kMaxSlabs) return fail(RRS_ERR_INVALID_ARGUMENT, "too many slabs");
   cudaError_t e = cudaEventRecord(comm->ev[8], st);  // the side stream starts after the prologue (and whatever
@@ -571,7 +577,7 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
     char* shard = static_cast<char*>(w.y_shard) + t0 * n_out_local * esz;
     rrs::GemmArgs a{w.Xq8 + t0 * K, w.x_scale + t0, w.s_group, Wq8, w_scale, ts, n_local, K, group, out_scale, false,
                     e4m3, shard, y_dtype, n_out_local, nullptr, swiglu};
-    e = rrs::launch_gemm(a, nsm, st);
+    e = rrs::launch_gemm(a, nslab > 1 ? nsm - kNcclCtas : nsm, st);  // leave SMs to the overlapping all-gather
     if (e != cudaSuccess) { status = cuda_fail(e, "rrs_gemm kernel"); break; }
     e = cudaEventRecord(comm->ev[sl], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(comm->side, comm->ev[sl], 0);
@@ -620,7 +626,12 @@ rrs_status rrs_comm_init(rrs_comm_t* comm, int32_t rank, int32_t world, const ui
   ncclUniqueId u;
   memcpy(&u, id, 128);
   auto* c = new rrs_comm_s{};
-  ncclResult_t r = ncclCommInitRank(&c->nccl, world, u, rank);
+  // NCCL kernels use at most kNcclCtas SMs; the slab GEMMs that overlap them leave that many SMs free (below), so
+  // the all-gather of slab s really runs concurrently with the GEMM of slab s+1
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.maxCTAs = kNcclCtas;
+  cfg.minCTAs = 1;
+  ncclResult_t r = ncclCommInitRankConfig(&c->nccl, world, u, rank, &cfg);
   if (r != ncclSuccess) {
     delete c;
     return fail(RRS_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
@@ -663,6 +674,21 @@ rrs_status rrs_debug_rotate(const void* X, int64_t T, int64_t K, float* Xr, floa
   if (e != cudaSuccess) return cuda_fail(e, "memset");
   e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr, nsm, st);
   return e == cudaSuccess ? RRS_OK : cuda_fail(e, "fwht_colmax_kernel");
+}
+
+rrs_status rrs_debug_relayout(const void* gathered, int64_t T, int64_t n_shard, int32_t world, int32_t y_dtype,
+                              void* Y, int64_t ldy, void* stream) {
+  g_last_error.clear();
+  int nsm;
+  if (rrs_status s = check_arch(nsm)) return s;
+  if (T < 0 || n_shard < 1 || world < 1 || ldy < n_shard * world || (y_dtype != RRS_BF16 && y_dtype != RRS_F32))
+    return fail(RRS_ERR_INVALID_ARGUMENT, "shape");
+  if (T == 0) return RRS_OK;
+  const int esz = y_dtype == RRS_F32 ? 4 : 2;
+  if (!gathered || !Y || !aligned16(gathered) || !aligned16(Y) || (n_shard * esz) % 16 || (ldy * esz) % 16)
+    return fail(RRS_ERR_MISALIGNED, "16-byte aligned buffers, shard width and ldy required");
+  cudaError_t e = rrs::launch_relayout_shards(gathered, Y, T, n_shard, world, ldy, esz, static_cast<cudaStream_t>(stream));
+  return e == cudaSuccess ? RRS_OK : cuda_fail(e, "relayout_kernel");
 }
 
 rrs_status rrs_debug_group_partials(const uint8_t* Xop, const uint8_t* Wop, int64_t T, int64_t N, int64_t K,

@@ -65,8 +65,8 @@ struct Cfg {
   static constexpr int X_STAGE = TP * KBLK;   // int8 X codes per K-block (SWIZZLE_128B tile)
   static constexpr int X_OFF = NS * W_STAGE;
   static constexpr int RING = X_OFF + NX * X_STAGE;
-  static constexpr int RED = TP * ROWS * 4;   // cluster reduction slots [S][TP][256/S] f32, overlaid on the W ring
-  static constexpr int SMEM = 1024 + RING + 1024 + MAX_G * 4;
+  static constexpr int RED = (TP + 4) * ROWS * 4;  // cluster reduction slots [S][256/S][TP + 4] f32, on the W ring
+  static constexpr int SMEM = 1024 + RING + 1024 + MAX_G * 4 + 64 * 4 + ROWS * 4;  // + s_g, alpha_t, beta_n
   static_assert(X_STAGE % 1024 == 0 && W_STAGE % 1024 == 0, "1024-byte aligned swizzle atoms");
   static_assert(RED <= NS * W_STAGE, "reduction overlay");
   static_assert(SMEM <= 227 * 1024, "shared memory");
@@ -108,6 +108,8 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   uint64_t* tempty = tfull + 2;
   uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* s_sm = reinterpret_cast<float*>(smem + C::RING + 1024);
+  float* xs_sm = s_sm + MAX_G;   // alpha_t * out_scale, t < T
+  float* ws_sm = xs_sm + 64;     // beta_n of this CTA's 256 rows (0 past N)
   float* red = reinterpret_cast<float*>(wring);           // after the K loop
 
   const uint32_t warp = ptx::warp_idx();
@@ -244,6 +246,11 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     ptx::pdl_wait();  // s_g come from the prologue
     for (int g = threadIdx.x - PROM0 * 32; g < ng; g += NPROM * 32) s_sm[g] = p.s_group[g0 + g];
+    {  // the epilogue's scales, read once here (off the critical path)
+      const int i = threadIdx.x - PROM0 * 32;  // 0 .. 255
+      if (i < p.T) xs_sm[i] = p.x_scale[i] * p.out_scale;
+      ws_sm[i] = row0 + i < p.N ? p.w_scale[row0 + i] : 0.0f;
+    }
     asm volatile("bar.sync 1, %0;" ::"n"(NPROM * 32));
     float acc[TP];  // sum_g s_g P_g of this thread's W row for the TP token columns
 #pragma unroll
@@ -275,15 +282,16 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       ptx::cluster_sync_warps_arrive();
       ptx::cluster_wait();
     }
-    // push this row's partials to the CTA that owns the row (rank r / rows_per): slot [my rank][t][r % rows_per]
+    // push this row's partials to the CTA that owns the row (rank r / rows_per): slot [my rank][r % rows_per][t],
+    // 16-byte stores (row stride TP + 4 floats: 16-byte aligned, and the reducer's float4 reads are conflict-free)
     const int r = h * 128 + q * 32 + lane;
-    float* dst = red + ((int)rank * TP) * rows_per + (r % rows_per);
+    float* dst = red + ((int)rank * rows_per + (r % rows_per)) * (TP + 4);
     const uint32_t owner = (uint32_t)(r / rows_per);
 #pragma unroll
-    for (int t = 0; t < TP; ++t) {
-      if (t < p.T) {
-        if (S > 1) ptx::st_dsmem_f32(dst + t * rows_per, owner, acc[t]);
-        else dst[t * rows_per] = acc[t];
+    for (int t4 = 0; t4 < TP / 4; ++t4) {
+      if (4 * t4 < p.T) {
+        if (S > 1) ptx::st_dsmem_v4(dst + 4 * t4, owner, acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
+        else *reinterpret_cast<float4*>(dst + 4 * t4) = make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
       }
     }
   }
@@ -298,16 +306,27 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   // ---- fixed-order reduction over the S slots (ranks 0..S-1) and the epilogue: rank r writes rows
   // [r 256/S, (r+1) 256/S) of the row block
   {
-    const int nout = p.T * rows_per;
+    const int nout = ((p.T + 3) / 4) * rows_per;  // (4 tokens, 1 row) per item
     for (int idx = threadIdx.x; idx < nout; idx += THREADS) {
-      const int t = idx / rows_per, rr = idx % rows_per;
+      const int tg = idx / rows_per, rr = idx % rows_per;
       const int n = row0 + (int)rank * rows_per + rr;
-      float sum = 0.0f;
-      for (int src = 0; src < S; ++src) sum += red[(src * TP + t) * rows_per + rr];
+      float4 sum = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      for (int src = 0; src < S; ++src) {
+        const float4 v = *reinterpret_cast<const float4*>(red + (src * rows_per + rr) * (TP + 4) + 4 * tg);
+        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+      }
       if (n < p.N) {
-        const float y = sum * (__ldg(p.x_scale + t) * p.out_scale) * __ldg(p.w_scale + n);
-        if (p.y_f32) reinterpret_cast<float*>(p.Y)[(int64_t)t * p.ldy + n] = y;
-        else reinterpret_cast<__nv_bfloat16*>(p.Y)[(int64_t)t * p.ldy + n] = __float2bfloat16_rn(y);
+        const float bn = ws_sm[(int)rank * rows_per + rr];
+        const float sv[4] = {sum.x, sum.y, sum.z, sum.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int t = 4 * tg + i;
+          if (t < p.T) {
+            const float y = sv[i] * xs_sm[t] * bn;
+            if (p.y_f32) reinterpret_cast<float*>(p.Y)[(int64_t)t * p.ldy + n] = y;
+            else reinterpret_cast<__nv_bfloat16*>(p.Y)[(int64_t)t * p.ldy + n] = __float2bfloat16_rn(y);
+          }
+        }
       }
     }
   }

@@ -50,11 +50,12 @@ bool prologue_fused_supports_k(int64_t K);
 cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
                                   unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,
                                   float* scale, bool e4m3, int group, int nsm, cudaStream_t st);
-// Decode-sized T (1..64, K = 2^m in [1024, 16384]): FWHT spread over T * K/1024 warps, X~ and chan_max written
-// (no memset needed); follow with launch_smooth_quant.
-bool prologue_small_supports(int64_t T, int64_t K);
-cudaError_t launch_prologue_small(const uint16_t* X, int64_t T, int64_t K, float* Xr, float* chan_max, int nsm,
-                                  cudaStream_t st);
+// Decode-sized T (1..64, K = 2^m in [1024, 8192]): rows a1-a6 in one cooperative launch, one CTA per row, the FWHT
+// of a row spread over its K/1024 warps; no memset (chan_max is written, not accumulated).  scratch: >= T * K f32.
+bool prologue_decode_supports(int64_t T, int64_t K, int group);
+cudaError_t launch_prologue_decode(const uint16_t* X, int64_t T, int64_t K, const int32_t* perm, unsigned* chan_max_bits,
+                                   float* scratch, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3,
+                                   int group, cudaStream_t st);
 // X~ = X (bf16 -> f32, no rotation) and, unless chan_max_bits is null, the runtime channel max (atomicMax on
 // zeroed float bits) -- the RRS_NO_ROTATION / RRS_PREROTATED prologue and the NO_ROTATION weight path
 cudaError_t launch_convert_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr, int nsm,

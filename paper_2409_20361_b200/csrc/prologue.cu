@@ -22,7 +22,7 @@ namespace rrs {
 // Optional per-CTA timeline (bench/micro/prologue_trace.cu builds this file with -DRRS_TRACE): thread 0
 // records %globaltimer at fixed points into g_trace[kernel][cta][slot].
 #ifdef RRS_TRACE
-__device__ unsigned long long g_trace[2][1024][16];
+__device__ unsigned long long g_trace[3][1024][16];
 RRS_DEVICE void trace(int k, int slot) {
   if (threadIdx.x == 0 && blockIdx.x < 1024 && slot < 16) {
     unsigned long long t;
@@ -384,19 +384,89 @@ prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __res
   ptx::pdl_launch_dependents();
 }
 
-// ------------------------------------------------------------------------------ a1 + a2, decode-sized T
+// ------------------------------------------------------------------------------ a1-a6, decode-sized T
 //
-// Small-T prologue (T <= 64, K = C * 1024, the decode regime of configs[3]): latency, not throughput, decides, so
-// the FWHT of every row is spread over C independent warps.  H_K = H_C (x) H_1024 (index i = 1024 a + b), and the
-// butterfly stages commute, so warp (t, c) computes output chunk c of row t on its own:
-//   v[b] = sum_a (-1)^popcount(a & c) x[t][1024 a + b]       (the H_C mix, read straight from global memory)
-//   y[1024 c + .] = FWHT_1024(v)                              (5 bits in registers, one warp-private transpose,
-//                                                              5 bits in registers)
-// Every intermediate is a signed subset sum of the row's inputs, so it is exact in fp64 under R3 and the single
-// rounding to f32 gives the correctly rounded X~ (bit-identical to fwht_colmax_kernel).  X~ goes to the workspace;
-// after one grid barrier (cooperative launch; counters in library-owned memory, self-cleaning, so no memset) the
-// grid reduces c_j = max_t |X~_tj| column by column (no atomics).  The quantisation pass is smooth_quant_kernel,
-// chained with programmatic dependent launch.
+// Decode prologue (T <= 64, K = C * 1024, the decode regime of configs[3]): latency, not throughput, decides.  One
+// CTA per token row, K/32 threads = C warps:
+//   * FWHT: H_K = H_C (x) H_1024 (index i = 1024 a + b) and the butterfly stages commute, so warp c computes output
+//     chunk c of the row on its own: v[b] = sum_a (-1)^popcount(a & c) x[1024 a + b] (the H_C mix, read straight from
+//     global memory), then FWHT_1024(v) with 5 bits in registers, one warp-private transpose, 5 bits in registers.
+//     Every intermediate is a signed subset sum of the row, exact in fp64 under R3; one rounding to f32 gives the
+//     correctly rounded X~ (bit-identical to fwht_colmax_kernel).  X~ stays in shared memory.
+//   * channel max over all T rows (Eq. 1, R6): CTA 0 zeroes chan_max, grid barrier, one atomicMax per column
+//     per row, grid barrier (cooperative launch; barrier counters in library memory, self-cleaning: no memset).
+//     T = 1 needs neither: chan_max = |X~| of the single row.
+//   * a3-a6 as in the prefill path (quant_row) on the shared-memory row.
+// FWHT of one bf16 row xrow[C * 1024] (shared memory) by the C warps of a CTA, each input converted to fp64 once.
+// H_K = H_C (x) H_1024 (index i = 1024 a + b); the butterfly stages commute:
+//   phase A: warp c transforms chunk c (b bits): 5 bits in registers, a warp-private transpose (tw, 32 x 33), 5 bits;
+//            lane l of warp c then holds chunk c at positions 32 j + l (j < 32), stored to y1[1024 c + 32 j + l].
+//   phase B: thread tid takes the nb = 32 / C positions b = nb tid .. nb tid + nb - 1 of all C chunks (32 values)
+//            and applies H_C across the chunks (a bits); out(i, value) receives every final y[i] exactly once.
+// Every intermediate is a signed subset sum of the row: exact in fp64 under R3.  Lane l reads its four 16-byte slots
+// of chunk c in the order q ^ rot, rot = (l >> 1) & 3 (a quarter-warp's loads hit 8 distinct bank groups), so
+// register k starts with the input at position k ^ m, m = 8 rot; the register butterflies then give
+// z[k] = sum_k' (-1)^(k.k') x[k' ^ m] = (-1)^popcount(k & m) y[k], whose sign the transpose store removes (exact).
+// Contains __syncthreads (every thread of the CTA must call it).
+template <int C, class Out>
+RRS_DEVICE void row_fwht_two_level(const uint16_t* xrow, double* tr, double* y1, Out&& out) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rot = (lane >> 1) & 3;
+  double v[32];
+  {  // phase A
+    const uint4* src = reinterpret_cast<const uint4*>(xrow + warp * 1024 + lane * 32);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 w = src[q ^ rot];
+      const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {  // bf16 -> f32 (bits) -> f64, exact
+        v[q * 8 + 2 * h] = (double)__uint_as_float(ws[h] << 16);
+        v[q * 8 + 2 * h + 1] = (double)__uint_as_float(ws[h] & 0xFFFF0000u);
+      }
+    }
+    butterflies<5>(v);
+    double* tw = tr + warp * (32 * 33);
+#pragma unroll
+    for (int e = 0; e < 32; ++e) tw[e * 33 + lane] = (__popc((e >> 3) & rot) & 1) ? -v[e] : v[e];
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = tw[lane * 33 + j];
+    butterflies<5>(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) y1[warp * 1024 + 32 * j + lane] = v[j];
+  }
+  __syncthreads();
+  if constexpr (C == 1) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out(32 * j + lane, v[j]);
+  } else {  // phase B: v[a * nb + i] = chunk a at position nb tid + i
+    constexpr int nb = 32 / C, lg = ilog2_c(C);
+    const int b0 = nb * threadIdx.x;
+#pragma unroll
+    for (int a = 0; a < C; ++a)
+#pragma unroll
+      for (int i = 0; i < nb; ++i) v[a * nb + i] = y1[a * 1024 + b0 + i];
+    // H_C over a: butterflies on the register bits above log2(nb)
+#pragma unroll
+    for (int hb = 0; hb < lg; ++hb) {
+      const int h = nb << hb;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) {
+        if ((k & h) == 0) {
+          const double x0 = v[k], x1 = v[k + h];
+          v[k] = x0 + x1;
+          v[k + h] = x0 - x1;
+        }
+      }
+    }
+#pragma unroll
+    for (int a = 0; a < C; ++a)
+#pragma unroll
+      for (int i = 0; i < nb; ++i) out(a * 1024 + b0 + i, v[a * nb + i]);
+  }
+}
+
 __device__ unsigned g_small_bar[256][2];  // [slot][arrive, depart]: zero at module load, reset by the last departer
 
 RRS_DEVICE void grid_barrier_selfclean(unsigned* bar, unsigned nblocks) {
@@ -417,98 +487,180 @@ RRS_DEVICE void grid_barrier_selfclean(unsigned* bar, unsigned nblocks) {
 }
 
 template <int C>
-__global__ void __launch_bounds__(128)
-prologue_small_kernel(const uint16_t* __restrict__ X, int T, float* __restrict__ Xr, float* __restrict__ chan_max,
-                      unsigned* __restrict__ bar) {
-  constexpr int K = C * 1024;
-  __shared__ double tr[4][32 * 33];  // warp-private 32 x 32 transpose (row stride 33)
-  ptx::pdl_launch_dependents();      // the quantisation kernel may get resident now (it waits for our completion)
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (u < T * C) {
-    const int t = u / C, c = u % C;
-    const uint16_t* row = X + (int64_t)t * K + lane * 32;
-    double v[32];
+struct DecodePrologueSmem {
+  static constexpr int K = C * 1024;
+  static constexpr int TR = C * 32 * 33 * 8;  // warp-private 32 x 32 fp64 transposes (row stride 33); later X~ row f32
+  static constexpr int Y1 = K * 8;            // phase-A results (fp64); later chan_max f32
+  static constexpr int XB = K * 2;            // the bf16 input row (one bulk copy)
+  static constexpr int BYTES = TR + Y1 + XB + 64 * 4 + 16;
+  static_assert(TR >= K * 4 && Y1 >= K * 4, "overlays");
+};
+
+// One CTA per token row (T <= 64), clusters of up to 8 CTAs (8 rows).  c_j = max over all T rows: the cluster reduces
+// its rows through DSMEM (CTA r takes columns [r K/8, (r+1) K/8)) into a per-cluster partial in `scratch`
+// ([clusters][K] f32: the workspace's X~ region, unused on this path), one grid barrier (counters in library memory,
+// self-cleaning: no memset), then every CTA takes the max over the cluster partials.  T = 1 needs none of it.
+template <int C>
+__global__ void __launch_bounds__(C * 32)
+prologue_decode_kernel(const uint16_t* __restrict__ X, int T, const int32_t* __restrict__ perm,
+                       unsigned* __restrict__ chan_max_bits, float* __restrict__ scratch, float* __restrict__ s_group_out,
+                       uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8, float* __restrict__ scale_out, int e4m3,
+                       int group, unsigned* __restrict__ bar) {
+  constexpr int K = C * 1024, TPR = K / 32;
+  using S = DecodePrologueSmem<C>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  double* tr = reinterpret_cast<double*>(smem);
+  double* y1 = reinterpret_cast<double*>(smem + S::TR);
+  float* xs = reinterpret_cast<float*>(smem);          // X~ row (natural column order), after phase A
+  float* cms = reinterpret_cast<float*>(smem + S::TR);  // chan_max, after phase B
+  uint16_t* xrow = reinterpret_cast<uint16_t*>(smem + S::TR + S::Y1);
+  float* red = reinterpret_cast<float*>(smem + S::TR + S::Y1 + S::XB);
+  uint64_t* bar_x = reinterpret_cast<uint64_t*>(smem + S::TR + S::Y1 + S::XB + 64 * 4);
+  ptx::pdl_launch_dependents();  // the decode GEMM may get resident (and start its W stream) on the SMs left free
+  const int tid = threadIdx.x;
+  const int t = blockIdx.x;
+  const bool live = t < T;  // the grid is padded to whole clusters
+  const int j0 = tid * 32;
+  if (tid == 0) {  // the whole bf16 row in one bulk copy
+    ptx::mbar_init(bar_x, 1);
+    ptx::fence_barrier_init();
+    if (live) {
+      ptx::mbar_arrive_expect_tx(bar_x, S::XB);
+      ptx::bulk_load(xrow, X + (int64_t)t * K, S::XB, bar_x);
+    }
+  }
+  trace(2, 0);
+  int pj[32];
+  load_perm32(perm, j0, pj);  // an offline input
+  __syncthreads();
+  if (live) ptx::mbar_wait(bar_x, 0);
+  else
+    for (int i = tid; i < K / 2; i += TPR) reinterpret_cast<uint32_t*>(xrow)[i] = 0u;  // a zero row: |X~| = 0
+  __syncthreads();
+  trace(2, 1);
+  // ---- a1 (X~ rounded once to f32, natural column order, into xs over the idle transposes)
+  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i] = __double2float_rn(d); });
+  __syncthreads();
+  trace(2, 2);
+  // ---- a2: c_j = max over all T rows
+  if (gridDim.x > 1) {
+    // (1) cluster max over its 8 rows: CTA r reduces columns [r K/8, (r+1) K/8) (one float4 of 4 columns per thread
+    //     and peer, all 8 DSMEM loads in flight) into the cluster partial in scratch
+    ptx::cluster_sync();  // every CTA's xs is complete
+    const uint32_t rank = ptx::cluster_ctarank();
+    constexpr int SL = K / 8;                // columns per rank
+    static_assert(SL / 4 <= TPR, "one float4 per thread");
+    const int ncl = (int)(gridDim.x / 8);
+    const int col4 = (int)rank * SL + 4 * tid;  // this thread's 4 columns (tid < SL / 4)
+    if (tid < SL / 4) {
+      float4 v[8];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) v[e] = 0.0;
+      for (uint32_t r = 0; r < 8; ++r) v[r] = ptx::ld_dsmem_f32x4(xs + col4, r);
+      float4 m = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
-    for (int a = 0; a < C; ++a) {
-      const bool neg = __popc(a & c) & 1;
-      const uint4* src = reinterpret_cast<const uint4*>(row + a * 1024);
+      for (int r = 0; r < 8; ++r) {
+        m.x = fmaxf(m.x, fabsf(v[r].x)); m.y = fmaxf(m.y, fabsf(v[r].y));
+        m.z = fmaxf(m.z, fabsf(v[r].z)); m.w = fmaxf(m.w, fabsf(v[r].w));
+      }
+      *reinterpret_cast<float4*>(scratch + (int64_t)(blockIdx.x / 8) * K + col4) = m;
+    }
+    __threadfence();
+    ptx::cluster_sync();  // peers are done reading this CTA's xs
+    grid_barrier_selfclean(bar, gridDim.x);
+    // (2) the same slice over all clusters (ncl float4 loads in flight per thread), into this CTA's cms slice
+    if (tid < SL / 4) {
+      float4 m = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      for (int q0 = 0; q0 < ncl; q0 += 8) {
+        float4 v[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const uint4 w = __ldg(src + q);
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+        for (int q = 0; q < 8; ++q)
+          v[q] = q0 + q < ncl ? __ldcg(reinterpret_cast<const float4*>(scratch + (int64_t)(q0 + q) * K + col4))
+                              : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-          const double lo = (double)__uint_as_float(ws[h] << 16), hi = (double)__uint_as_float(ws[h] & 0xFFFF0000u);
-          v[q * 8 + 2 * h] = neg ? v[q * 8 + 2 * h] - lo : v[q * 8 + 2 * h] + lo;
-          v[q * 8 + 2 * h + 1] = neg ? v[q * 8 + 2 * h + 1] - hi : v[q * 8 + 2 * h + 1] + hi;
+        for (int q = 0; q < 8; ++q) {
+          m.x = fmaxf(m.x, v[q].x); m.y = fmaxf(m.y, v[q].y); m.z = fmaxf(m.z, v[q].z); m.w = fmaxf(m.w, v[q].w);
         }
       }
+      *reinterpret_cast<float4*>(cms + col4) = m;
+      if (blockIdx.x < 8) *reinterpret_cast<float4*>(chan_max_bits + col4) = m;  // float bits (>= +0)
     }
-    butterflies<5>(v);  // bits 0..4 of the chunk position (= e)
-    double* S = tr[warp];
+    // (3) every CTA gathers the other seven slices from its cluster peers (all 8 loads in flight, then the stores)
+    ptx::cluster_sync();
+    {
+      constexpr int PER = K / 4 / TPR;  // 8 float4 per thread
+      float4 g[PER];
 #pragma unroll
-    for (int e = 0; e < 32; ++e) S[e * 33 + lane] = v[e];
-    __syncwarp();
+      for (int k = 0; k < PER; ++k) {
+        const int i = tid + k * TPR;
+        const uint32_t r = (uint32_t)(4 * i / SL);
+        g[k] = r != rank ? ptx::ld_dsmem_f32x4(cms + 4 * i, r) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = S[lane * 33 + j];  // now position 32 j + lane
-    butterflies<5>(v);  // bits 5..9
-    float* out = Xr + (int64_t)t * K + c * 1024 + lane;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) out[32 * j] = __double2float_rn(v[j]);
+      for (int k = 0; k < PER; ++k) {
+        const int i = tid + k * TPR;
+        if ((uint32_t)(4 * i / SL) != rank) *reinterpret_cast<float4*>(cms + 4 * i) = g[k];
+      }
+    }
+    ptx::cluster_sync();  // no CTA exits (or overwrites cms) while a peer still reads it
+  } else {
+    for (int i = tid; i < K; i += TPR) {
+      cms[i] = fabsf(xs[i]);
+      chan_max_bits[i] = __float_as_uint(cms[i]);
+    }
   }
-  __threadfence();
-  grid_barrier_selfclean(bar, gridDim.x);
-  // c_j = max_t |X~_tj| (Eq. 1, over all T tokens of the call, R6), one column per thread
-  for (int col = blockIdx.x * blockDim.x + threadIdx.x; col < K; col += gridDim.x * blockDim.x) {
-    float m = 0.0f;
-    for (int t = 0; t < T; ++t) m = fmaxf(m, fabsf(__ldcg(Xr + (int64_t)t * K + col)));
-    chan_max[col] = m;
-  }
+  __syncthreads();
+  trace(2, 4);
+  // ---- a3-a6 on this CTA's row
+  const float inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0, s_group_out, group);
+  trace(2, 5);
+  if (live) quant_row<TPR>(xs, pj, inv_s, true, red, tid, 0, t, T, K, j0, Xq, Xq8, scale_out, e4m3 != 0, [] {});
+  trace(2, 6);
 }
 
 template <int C>
-static cudaError_t launch_small_k(const uint16_t* X, int64_t T, float* Xr, float* chan_max, unsigned slot, int nsm,
-                                  cudaStream_t st) {
-  auto kern = prologue_small_kernel<C>;
-  const int64_t units = T * C;
-  // one warp per unit; pack up to 4 warps per CTA only when there are more units than SMs
-  const int warps = units >= 4LL * nsm ? 4 : units >= 2LL * nsm ? 2 : 1;
-  const int grid = (int)((units + warps - 1) / warps);
+static cudaError_t launch_decode_prologue_k(const uint16_t* X, int64_t T, const int32_t* perm, unsigned* cm,
+                                            float* scratch, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale,
+                                            bool e4m3, int group, unsigned slot, cudaStream_t st) {
+  auto kern = prologue_decode_kernel<C>;
+  constexpr int smem = DecodePrologueSmem<C>::BYTES;
+  cudaError_t e = prepare_kernel(kern, smem, C * 32);
+  if (e != cudaSuccess) return e;
   void* bar = nullptr;
-  cudaError_t e = cudaGetSymbolAddress(&bar, g_small_bar);
+  e = cudaGetSymbolAddress(&bar, g_small_bar);
   if (e != cudaSuccess) return e;
   unsigned* b = static_cast<unsigned*>(bar) + 2 * (slot & 255u);
-  int Ti = (int)T;
+  int Ti = (int)T, ei = (int)e4m3;
+  const unsigned grid = T == 1 ? 1u : (unsigned)((T + 7) / 8 * 8);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(32 * warps);
-  cfg.dynamicSmemBytes = 0;
+  cfg.blockDim = dim3(C * 32);
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 8;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, X, Ti, Xr, chan_max, b);
+  cfg.numAttrs = grid > 1 ? 2 : 0;  // a single row needs neither (no barrier, no cluster)
+  return cudaLaunchKernelEx(&cfg, kern, X, Ti, perm, cm, scratch, s_group, Xq, Xq8, scale, ei, group, b);
 }
 
-bool prologue_small_supports(int64_t T, int64_t K) {
-  return T >= 1 && T <= 64 && K >= 1024 && K <= 16384 && (K & (K - 1)) == 0;
+bool prologue_decode_supports(int64_t T, int64_t K, int group) {
+  return T >= 1 && T <= 64 && K >= 1024 && K <= 8192 && (K & (K - 1)) == 0 && group >= 32;
 }
 
-cudaError_t launch_prologue_small(const uint16_t* X, int64_t T, int64_t K, float* Xr, float* chan_max, int nsm,
-                                  cudaStream_t st) {
+cudaError_t launch_prologue_decode(const uint16_t* X, int64_t T, int64_t K, const int32_t* perm, unsigned* chan_max_bits,
+                                   float* scratch, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3,
+                                   int group, cudaStream_t st) {
   static std::atomic<unsigned> calls{0};  // barrier slot per call: concurrent calls use different counters
   const unsigned slot = calls.fetch_add(1u, std::memory_order_relaxed);
   switch (K) {
-    case 1024: return launch_small_k<1>(X, T, Xr, chan_max, slot, nsm, st);
-    case 2048: return launch_small_k<2>(X, T, Xr, chan_max, slot, nsm, st);
-    case 4096: return launch_small_k<4>(X, T, Xr, chan_max, slot, nsm, st);
-    case 8192: return launch_small_k<8>(X, T, Xr, chan_max, slot, nsm, st);
-    case 16384: return launch_small_k<16>(X, T, Xr, chan_max, slot, nsm, st);
+#define RRS_CASE(c) case c * 1024: return launch_decode_prologue_k<c>(X, T, perm, chan_max_bits, scratch, s_group, Xq, Xq8, scale, e4m3, group, slot, st);
+    RRS_CASE(1) RRS_CASE(2) RRS_CASE(4) RRS_CASE(8)
+#undef RRS_CASE
     default: return cudaErrorInvalidValue;
   }
 }

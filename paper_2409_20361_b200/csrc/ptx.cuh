@@ -57,22 +57,39 @@ RRS_DEV uint32_t cluster_ctarank() {
 RRS_DEV void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-// 32-bit load from the shared memory of CTA `rank` of this cluster at the address of local `p`
-// (not volatile, no memory clobber: independent loads may be issued back to back; callers order them
-// against peer writes with cluster barriers)
+// 32-bit load from the shared memory of CTA `rank` of this cluster at the address of local `p` (volatile, so never
+// hoisted above the cluster barrier that orders it after the peer's writes; no memory clobber, so independent loads
+// are issued back to back)
 RRS_DEV uint32_t ld_dsmem_u32(const void* p, uint32_t rank) {
   uint32_t remote, v;
   asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
-  asm("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote));
   return v;
 }
-RRS_DEV float ld_dsmem_f32(const void* p, uint32_t rank) { return __uint_as_float(ld_dsmem_u32(p, rank)); }
+// 16-byte load from the shared memory of CTA `rank` of this cluster at the address of local `p` (16-byte aligned)
+RRS_DEV float4 ld_dsmem_f32x4(const void* p, uint32_t rank) {
+  uint32_t remote;
+  float4 v;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  // volatile (never hoisted above the cluster barrier that orders it after the peer's writes) but without a memory
+  // clobber: consecutive loads are issued back to back and stay in flight together
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(remote));
+  return v;
+}
 // 32-bit store into the shared memory of CTA `rank` of this cluster at the address of local `p` (weak; made
 // visible to that CTA by a following cluster barrier)
 RRS_DEV void st_dsmem_f32(void* p, uint32_t rank, float v) {
   uint32_t remote;
   asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
   asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
+}
+// 16-byte store into the shared memory of CTA `rank` (address of local `p`, 16-byte aligned)
+RRS_DEV void st_dsmem_v4(void* p, uint32_t rank, float a, float b, float c, float d) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
 }
 // the two halves of cluster_sync (arrive with release / wait with acquire), for warps that do work in between
 RRS_DEV void cluster_sync_warps_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
@@ -107,11 +124,6 @@ RRS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
 }
 
 // ------------------------------------------------------------------ TMA
-// bulk prefetch of [gaddr, gaddr + bytes) into L2 (16-byte aligned, bytes % 16 == 0); no completion tracking
-RRS_DEV void prefetch_l2_bulk(const void* gaddr, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(gaddr)), "r"(bytes)
-               : "memory");
-}
 RRS_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
 }
@@ -172,7 +184,6 @@ RRS_DEV void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;" ::
 RRS_DEV void bulk_wait_group_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 RRS_DEV void bulk_wait_group0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 RRS_DEV void fence_proxy_async_shared() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-constexpr uint64_t kEvictFirst = 0x12F0000000000000ull;
 constexpr uint64_t kEvictLast = 0x14F0000000000000ull;
 constexpr uint64_t kEvictNormal = 0x1000000000000000ull;
 
@@ -269,19 +280,6 @@ RRS_DEV void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-// 32 lanes x 32 columns of 32-bit: each thread gets its lane's 32 consecutive columns
-#define RRS_TMEM_LD32(taddr, r)                                                                          \
-  asm volatile(                                                                                         \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"  \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                          \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),  \
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),        \
-        "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),      \
-        "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),      \
-        "=r"(r[29]), "=r"(r[30]), "=r"(r[31])                                                           \
-      : "r"(taddr))
-
-// 32 lanes x 32 columns of 32-bit, every column of every lane set to the same value v
 // 32 lanes x 16 columns of 32-bit
 #define RRS_TMEM_LD16(taddr, r)                                                                          \
   asm volatile(                                                                                         \
@@ -300,11 +298,6 @@ RRS_DEV void mma_commit(uint64_t* bar) {
                  "+r"(r[14]), "+r"(r[15])                                                                \
                :                                                                                         \
                : "memory")
-
-#define RRS_TMEM_ST32_SPLAT(taddr, v)                                                                    \
-  asm volatile(                                                                                         \
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,"   \
-      "%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v) : "memory")
 
 #define RRS_TMEM_ST16_SPLAT(taddr, v)                                                                    \
   asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" \
@@ -327,21 +320,6 @@ RRS_DEV void mma_commit(uint64_t* bar) {
                : "memory")
 
 RRS_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
-
-// packed FP32 pair arithmetic (sm_100): d = a + b, d = a * b + c, elementwise on (lo, hi)
-RRS_DEV uint64_t f32x2_add(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-RRS_DEV uint64_t f32x2_fma(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-RRS_DEV uint64_t pack2(uint32_t lo, uint32_t hi) { return ((uint64_t)hi << 32) | lo; }
-
-RRS_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // Shared-memory matrix descriptor (tcgen05 "matrix descriptor"):
 //   [0,14) start address >> 4 | [16,30) leading byte offset >> 4 | [32,46) stride byte offset >> 4

@@ -74,6 +74,8 @@ WORKLOADS = {
     "c4_decode_t64": Workload("c4_decode_t64", 64, 8192, 8192, "mixed", note="configs[3]"),
     "c4_decode_t1": Workload("c4_decode_t1", 1, 8192, 8192, "mixed", note="configs[3]"),
     "c5_llama3_70b_up": Workload("c5_llama3_70b_up", 8192, 8192, 28672, "channel", note="configs[4]"),
+    "c5_llama3_70b_up_rank8": Workload("c5_llama3_70b_up_rank8", 8192, 8192, 3584, "channel",
+                                       note="configs[4] per-rank shard at P=8 (N/8 = 3584), one GPU"),
 }
 
 

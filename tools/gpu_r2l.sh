@@ -1,0 +1,7 @@
+cd $GRAFT_REPO_ROOT
+TAG=${TAG:-r2l}
+./tools/decode_trace 64 > gpurun_out/dtrace_${TAG}.txt 2>&1
+for a in "1 8192 2" "64 8192 2" "16 8192 2"; do echo "== prologue_trace $a"; timeout 60 ./bench/micro/prologue_trace $a; done > gpurun_out/ptrace_${TAG}.txt 2>&1
+timeout 300 python tools/time_decode.py 1 16 64 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_decode.py tests/test_gpu_parity_r2.py tests/test_gpu_variants.py -q -m gpu --timeout 400 -x -k "decode or K_extremes or prologue" > gpurun_out/pytest_${TAG}.txt 2>&1; echo pytest rc=$?; tail -8 gpurun_out/pytest_${TAG}.txt
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu --timeout 400 -x -k "prologue_bitexact" > gpurun_out/pytest2_${TAG}.txt 2>&1; echo pytest2 rc=$?; tail -3 gpurun_out/pytest2_${TAG}.txt
