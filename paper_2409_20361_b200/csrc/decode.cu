@@ -65,10 +65,13 @@ struct Cfg {
   static constexpr int X_STAGE = TP * KBLK;   // int8 X codes per K-block (SWIZZLE_128B tile)
   static constexpr int X_OFF = NS * W_STAGE;
   static constexpr int RING = X_OFF + NX * X_STAGE;
-  static constexpr int RED = (TP + 4) * ROWS * 4;  // cluster reduction slots [S][256/S][TP + 4] f32, on the W ring
+  static constexpr int ROWB = (TP + 4) * 4;      // one row of partials (f32, 16-byte aligned stride)
+  // after the K loop, on the ring: this CTA's partials [256][TP + 4] f32, then the S incoming slots
+  // [S][256/S][TP + 4] (the same 256 rows' worth of bytes)
+  static constexpr int RED = 2 * ROWS * ROWB;
   static constexpr int SMEM = 1024 + RING + 1024 + MAX_G * 4 + 64 * 4 + ROWS * 4;  // + s_g, alpha_t, beta_n
   static_assert(X_STAGE % 1024 == 0 && W_STAGE % 1024 == 0, "1024-byte aligned swizzle atoms");
-  static_assert(RED <= NS * W_STAGE, "reduction overlay");
+  static_assert(RED <= RING, "reduction overlay");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
 }  // namespace dec
@@ -106,11 +109,13 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   uint64_t* aempty = afull + NA;
   uint64_t* tfull = aempty + NA;
   uint64_t* tempty = tfull + 2;
-  uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* redbar = tempty + 2;     // the peers' partial slices have landed (bulk copies, complete_tx)
+  uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(redbar + 1);
   float* s_sm = reinterpret_cast<float*>(smem + C::RING + 1024);
   float* xs_sm = s_sm + MAX_G;   // alpha_t * out_scale, t < T
   float* ws_sm = xs_sm + 64;     // beta_n of this CTA's 256 rows (0 past N)
-  float* red = reinterpret_cast<float*>(wring);           // after the K loop
+  float* part = reinterpret_cast<float*>(wring);          // after the K loop: own partials [256][TP + 4]
+  float* slots = part + ROWS * (TP + 4);                   // incoming [S][256/S][TP + 4]
 
   const uint32_t warp = ptx::warp_idx();
   const int lane = threadIdx.x & 31;
@@ -142,6 +147,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], NPROM);
     }
+    ptx::mbar_init(redbar, 1);
     ptx::fence_barrier_init();
   }
   if (threadIdx.x == 0) dtrace(5, 0);
@@ -276,33 +282,39 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       }
     }
     // every MMA has completed (this warp saw the last tfull), so every converter and every ring stage of this CTA
-    // is done; the first cluster barrier makes the same true for the peers before anyone writes into their rings
-    ptx::tc_fence_before();
-    if (S > 1) {
-      ptx::cluster_sync_warps_arrive();
-      ptx::cluster_wait();
-    }
-    // push this row's partials to the CTA that owns the row (rank r / rows_per): slot [my rank][r % rows_per][t],
-    // 16-byte stores (row stride TP + 4 floats: 16-byte aligned, and the reducer's float4 reads are conflict-free)
+    // is done: the partials go to this CTA's own ring (16-byte stores, row stride TP + 4 floats), and a proxy fence
+    // makes them visible to the bulk copies below
+    if (warp == PROM0 && lane == 0) dtrace(7, 0);
     const int r = h * 128 + q * 32 + lane;
-    float* dst = red + ((int)rank * rows_per + (r % rows_per)) * (TP + 4);
-    const uint32_t owner = (uint32_t)(r / rows_per);
 #pragma unroll
-    for (int t4 = 0; t4 < TP / 4; ++t4) {
-      if (4 * t4 < p.T) {
-        if (S > 1) ptx::st_dsmem_v4(dst + 4 * t4, owner, acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
-        else *reinterpret_cast<float4*>(dst + 4 * t4) = make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
-      }
-    }
+    for (int t4 = 0; t4 < TP / 4; ++t4)
+      if (4 * t4 < p.T)
+        *reinterpret_cast<float4*>(part + r * (TP + 4) + 4 * t4) =
+            make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
+    ptx::fence_proxy_async_shared();
   }
-  if (S > 1 && (warp < PROM0 || warp == X_PROD)) {  // the other warps' half of the first cluster barrier
-    ptx::tc_fence_before();
-    ptx::cluster_sync_warps_arrive();
-    ptx::cluster_wait();
-  }
-  // second barrier: the pushes are visible to their owners
+  // first cluster barrier: every CTA of the cluster is done with its ring (the peers' slots are free) and has its
+  // partials in place
+  ptx::tc_fence_before();
   if (S > 1) ptx::cluster_sync();
   else __syncthreads();
+  if (warp == PROM0 && lane == 0) dtrace(7, 1);
+  // the owner of rows [r 256/S, (r+1) 256/S) is rank r: one bulk copy (TMA) per peer of that contiguous slice into the
+  // peer's slot [my rank], completing on the peer's redbar -- shared-memory-to-shared-memory over the cluster
+  const uint32_t slice_bytes = (uint32_t)(rows_per * (TP + 4) * 4);
+  if (threadIdx.x == 0 && S > 1) {
+    ptx::mbar_arrive_expect_tx(redbar, (uint32_t)(S - 1) * slice_bytes);
+    for (int o = 0; o < S; ++o) {
+      if (o == (int)rank) continue;
+      ptx::bulk_copy_cta_to_peer(slots + ((int)rank * rows_per) * (TP + 4), (uint32_t)o,
+                                 part + (o * rows_per) * (TP + 4), slice_bytes, redbar);
+    }
+  }
+  if (S > 1) {
+    ptx::mbar_wait(redbar, 0);  // the S - 1 incoming slices have landed
+    ptx::cluster_sync_warps_arrive();  // ... so every copy out of a peer's partials has completed (joined at the end)
+  }
+  if (threadIdx.x == 0) dtrace(7, 2);
   // ---- fixed-order reduction over the S slots (ranks 0..S-1) and the epilogue: rank r writes rows
   // [r 256/S, (r+1) 256/S) of the row block
   {
@@ -311,8 +323,10 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       const int tg = idx / rows_per, rr = idx % rows_per;
       const int n = row0 + (int)rank * rows_per + rr;
       float4 sum = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-      for (int src = 0; src < S; ++src) {
-        const float4 v = *reinterpret_cast<const float4*>(red + (src * rows_per + rr) * (TP + 4) + 4 * tg);
+      for (int src = 0; src < S; ++src) {  // fixed rank order (R15); this CTA's own slice straight from part
+        const float* row = src == (int)rank ? part + ((int)rank * rows_per + rr) * (TP + 4)
+                                            : slots + (src * rows_per + rr) * (TP + 4);
+        const float4 v = *reinterpret_cast<const float4*>(row + 4 * tg);
         sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
       }
       if (n < p.N) {
@@ -331,6 +345,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     }
   }
   if (threadIdx.x == 0) dtrace(6, 0);
+  if (S > 1) ptx::cluster_wait();  // no CTA exits while a peer's bulk copy may still read its partials
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();

@@ -547,6 +547,7 @@ prologue_decode_kernel(const uint16_t* __restrict__ X, int T, const int32_t* __r
     // (1) cluster max over its 8 rows: CTA r reduces columns [r K/8, (r+1) K/8) (one float4 of 4 columns per thread
     //     and peer, all 8 DSMEM loads in flight) into the cluster partial in scratch
     ptx::cluster_sync();  // every CTA's xs is complete
+    trace(2, 3);
     const uint32_t rank = ptx::cluster_ctarank();
     constexpr int SL = K / 8;                // columns per rank
     static_assert(SL / 4 <= TPR, "one float4 per thread");
@@ -564,9 +565,11 @@ prologue_decode_kernel(const uint16_t* __restrict__ X, int T, const int32_t* __r
       }
       *reinterpret_cast<float4*>(scratch + (int64_t)(blockIdx.x / 8) * K + col4) = m;
     }
-    __threadfence();
-    ptx::cluster_sync();  // peers are done reading this CTA's xs
+    trace(2, 7);
+    // (the grid barrier's fence in thread 0, after the CTA barrier, releases every thread's scratch stores; no peer
+    // ever writes xs, and the cluster barrier in (3) keeps every CTA alive until its peers' DSMEM reads are done)
     grid_barrier_selfclean(bar, gridDim.x);
+    trace(2, 9);
     // (2) the same slice over all clusters (ncl float4 loads in flight per thread), into this CTA's cms slice
     if (tid < SL / 4) {
       float4 m = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
@@ -585,7 +588,9 @@ prologue_decode_kernel(const uint16_t* __restrict__ X, int T, const int32_t* __r
       if (blockIdx.x < 8) *reinterpret_cast<float4*>(chan_max_bits + col4) = m;  // float bits (>= +0)
     }
     // (3) every CTA gathers the other seven slices from its cluster peers (all 8 loads in flight, then the stores)
+    trace(2, 10);
     ptx::cluster_sync();
+    trace(2, 11);
     {
       constexpr int PER = K / 4 / TPR;  // 8 float4 per thread
       float4 g[PER];

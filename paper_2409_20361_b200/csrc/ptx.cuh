@@ -145,6 +145,16 @@ RRS_DEV void bulk_load(void* smem_dst, const void* gmem_src, uint32_t bytes, uin
       "l"(reinterpret_cast<uint64_t>(gmem_src)), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// bulk copy (TMA engine) from this CTA's shared memory to the same-offset-mapped `dst_local` in CTA `rank` of the
+// cluster; completes `bytes` transaction bytes on that CTA's mbarrier at the offset of local `bar`.  16-byte aligned.
+RRS_DEV void bulk_copy_cta_to_peer(void* dst_local, uint32_t rank, const void* src, uint32_t bytes, uint64_t* bar) {
+  uint32_t dst, mb;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(dst) : "r"(smem_u32(dst_local)), "r"(rank));
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(mb) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(smem_u32(src)), "r"(bytes), "r"(mb)
+               : "memory");
+}
 // 2-D tiled load issued by either CTA of a tcgen05 CTA pair; `bar` is a shared::cluster address (may be
 // the peer CTA's mbarrier, e.g. the pair leader's).
 RRS_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, uint32_t bar_cluster_addr, int32_t c0, int32_t c1,

@@ -31,6 +31,14 @@ int main(int argc, char** argv) {
   static unsigned long long h[8][8][64];
   cudaMemcpyFromSymbol(h, rrs::g_dtrace, sizeof(h));
   const char* names[7] = {"W issued", "X issued", "converted", "MMA issued", "promoted", "start", "end"};
+  for (int c = 0; c < 8; ++c) {
+    unsigned long long t0 = h[0][5][0];
+    printf("CTA %d: start %.2f  first conv %.2f  last promoted %.2f  cl-wait1 %.2f  pushed %.2f  cl-sync2 %.2f  end %.2f us\n", c,
+           (double)(long long)(h[c][5][0] - t0) * 1e-3, (double)(long long)(h[c][2][0] - t0) * 1e-3,
+           (double)(long long)(h[c][4][15] - t0) * 1e-3, (double)(long long)(h[c][7][0] - t0) * 1e-3,
+           (double)(long long)(h[c][7][1] - t0) * 1e-3, (double)(long long)(h[c][7][2] - t0) * 1e-3,
+           (double)(long long)(h[c][6][0] - t0) * 1e-3);
+  }
   for (int c = 0; c < 2; ++c) {
     unsigned long long t0 = h[c][5][0];
     printf("CTA %d: start 0, end %.2f us\n", c, (h[c][6][0] - t0) * 1e-3);

@@ -59,6 +59,17 @@ def main():
         rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, ws=pws, i8=True)
         res["decode_gemm"] = timeit(lambda: rrs.rrs_gemm(Xop, xs, sg, layer.Wp4, layer.w_scale, Y, 1.0 / K,
                                                          packed4=True), flush)
+        # the same step replayed from a CUDA graph (how a serving loop launches decode steps)
+        gs = torch.cuda.Stream()
+        gs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(gs):
+            for _ in range(3):
+                rrs.rrs_linear(X, perm, layer.Wp4, layer.w_scale, Y, ws, N_total=N, packed4=True, stream=gs)
+        torch.cuda.current_stream().wait_stream(gs)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=gs):
+            rrs.rrs_linear(X, perm, layer.Wp4, layer.w_scale, Y, ws, N_total=N, packed4=True, stream=gs)
+        res["layer_packed4_graph"] = timeit(graph.replay, flush)
         gb = layer.Wp4.numel() / 1e9
         line = ", ".join(f"{k} {m:.2f} us (min {mn:.2f})" for k, (m, mn) in res.items())
         print(f"T={T}: {line}; decode GEMM W stream {gb / (res['decode_gemm'][0] * 1e-6):.0f} GB/s", flush=True)
