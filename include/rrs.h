@@ -32,8 +32,10 @@
  *     {7168, 14336} (28*2^m, R2); T >= 0; N >= 1.  All pointers 16-byte aligned.
  *   - X must be bf16 and satisfy the exactness precondition of DESIGN.md R3 (per row, exponent span
  *     of the nonzero |x| <= 45 - ceil(log2 K)); NaN/Inf inputs are undefined behaviour (not checked).
- *   - Reentrant; no global state besides the cached device properties and the NCCL communicator
- *     objects the caller creates.
+ *   - Reentrant.  Library state: per-device caches (device properties, occupancy, kernel attributes) behind a
+ *     mutex; the decode prologue's grid-barrier counters (256 slots in device memory, zero at load, reset by every
+ *     use, one slot per call from an atomic counter -- a CUDA graph captures its slot, so concurrent replays of ONE
+ *     graph on several streams are not supported); the NCCL communicator objects the caller creates.
  */
 #ifndef RRS_H_
 #define RRS_H_
@@ -184,7 +186,10 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
 rrs_status rrs_allgather_columns(const void* Y_shard, int64_t T, int64_t N_total, int32_t y_dtype, void* Y,
                                  int64_t ldy, rrs_comm_t comm, void* ws, size_t ws_bytes, void* stream);
 
-/* Communicator (NCCL over NVLink/NVSwitch).  torch.distributed only ferries the 128-byte id. */
+/* Communicator (NCCL over NVLink/NVSwitch).  torch.distributed only ferries the 128-byte id.  Collective calls
+ * (rrs_linear / rrs_allgather_columns with a communicator) validate every argument before joining a collective, so
+ * an argument error returns on the rank that made it; as with NCCL itself, arguments must agree across ranks or the
+ * other ranks block in the collective. */
 rrs_status rrs_comm_unique_id(uint8_t id[128]);
 rrs_status rrs_comm_init(rrs_comm_t* comm, int32_t rank, int32_t world, const uint8_t id[128]);
 rrs_status rrs_comm_destroy(rrs_comm_t comm);
