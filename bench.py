@@ -151,7 +151,6 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool, i8: bo
     Xop = torch.empty((T, K), dtype=torch.uint8, device=dev)
     xs = torch.empty(T, dtype=torch.float32, device=dev)
     sg = torch.empty(K // 128, dtype=torch.float32, device=dev)
-    cm = torch.empty(K, dtype=torch.float32, device=dev)
     pws = torch.empty(rrs.rrs_workspace_bytes(T, 1, K, 128, 1), dtype=torch.uint8, device=dev)
     Y_shard = torch.empty((T, n_local), dtype=out_dtype, device=dev)
     Y = torch.empty((T, N), dtype=out_dtype, device=dev)
@@ -202,8 +201,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool, i8: bo
     sub_ws = torch.rand((G, n_local), dtype=torch.float32, device=dev) + 0.5
     Xop_b, xs_b, sg_b = torch.empty_like(Xop), torch.empty_like(xs), torch.empty_like(sg)
     pieces = {
-        "prologue": lambda: rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, chan_max=cm, ws=pws, i8=op_i8,
-                                                        stream=stream),
+        "prologue": lambda: rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, ws=pws, i8=op_i8, stream=stream),
         "rrs_gemm": (lambda: rrs.rrs_gemm(Xop, xs, sg, layer.Wp4, layer.w_scale, Y_shard, out_scale, packed4=True,
                                           stream=stream)) if decode else
                     (lambda: rrs.rrs_gemm(Xop, xs, sg, layer.Wop, layer.w_scale, Y_shard, out_scale, i8=i8,
@@ -225,7 +223,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool, i8: bo
         pieces["r1_byte_operand_layer"] = lambda: rrs.rrs_linear(X, perm, layer.Wop, layer.w_scale, Y, ws, N_total=N,
                                                                  stream=stream)
     times = {k: [] for k in pieces}
-    rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, chan_max=cm, ws=pws, i8=op_i8, stream=stream)
+    rrs.rrs_rotate_smooth_quant(X, perm, None, Xop, xs, sg, ws=pws, i8=op_i8, stream=stream)
     for i in range(args.warmup + args.steps):
         evp = {k: new_events(1, 2)[0] for k in pieces}
         for k, fn in pieces.items():
@@ -447,10 +445,10 @@ def run_gpu(args):
                 "d2h_bytes_per_step": head["d2h"],
                 "api": "rrs_linear (pinned host X -> device -> host Y, copies inside the timed region)"},
         "gpu_launches": (2 if pow2 else 3) + (1 if world > 1 else 0),
-        "gpu_launches_note": "per step: " + ("prologue_fused_kernel" if pow2 else "fwht_colmax_kernel, smooth_quant_kernel")
+        "gpu_launches_note": "per step: " + ("prologue_group_kernel" if pow2 else
+                                             "fwht_colmax_kernel, smooth_quant_kernel (+ one cudaMemsetAsync of chan_max)")
                              + ", rrs_gemm_kernel"
-                             + (", relayout_kernel (+ ncclAllGather)" if world > 1 else "")
-                             + " (+ one cudaMemsetAsync of chan_max)",
+                             + (", relayout_kernel (+ ncclAllGather)" if world > 1 else ""),
         "clocks": head["clocks"],
         "wall_s_timed_region": head["wall_s_timed_region"],
     }

@@ -45,7 +45,7 @@ int main(int argc, char** argv) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    rrs::launch_prologue_fused(X, T, K, cm, Xr, counter, perm, sg, nullptr, q, sc, true, 128, nsm, 0);
+    rrs::launch_prologue_fused(X, T, K, Xr, perm, sg, nullptr, q, sc, true, 128, 0);
     cudaEventRecord(e1);
     cudaError_t e = cudaDeviceSynchronize();
     float a;

@@ -128,7 +128,10 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
  * X: device bf16 bits [T][K]; perm: device int32 [K];
  * outputs: Xq uint8 [T][K/2] (nullable), Xop uint8 [T][K] GEMM operand (nullable; flags as for
  *          rrs_prepare_weights), x_scale f32 [T],
- *          s_group f32 [K/group], chan_max f32 [K] (nullable: then taken from ws).
+ *          s_group f32 [K/group], chan_max f32 [K] (nullable).  Without chan_max the prefill prologue for
+ *          K = 2^m (T > 64) is one cooperative launch that reduces the group maxima s_g directly (the max over
+ *          tokens and the group's channels jointly, identical by construction); with chan_max it runs the rotate
+ *          and quantise passes as two kernels.  Both give identical s_group, x_scale and codes.
  * ws: device scratch, 16-byte aligned, >= rrs_workspace_bytes(T, 1, K, group, 1) bytes (holds X~). */
 rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, int64_t K, int32_t group,
                                    const int32_t* perm, uint8_t* Xq, uint8_t* Xop, float* x_scale,

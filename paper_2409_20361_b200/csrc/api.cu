@@ -123,7 +123,7 @@ size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t
   Workspace tmp;
   Workspace& ws = w ? *w : tmp;
   ws.Xr = static_cast<float*>(take(sizeof(float) * (size_t)T * K));
-  ws.chan_max = static_cast<float*>(take(sizeof(float) * (K + 64)));  // [K] + the fused prologue's CTA counter
+  ws.chan_max = static_cast<float*>(take(sizeof(float) * K));
   ws.s_group = static_cast<float*>(take(sizeof(float) * (K / group)));
   ws.x_scale = static_cast<float*>(take(sizeof(float) * (T > 0 ? T : 1)));
   ws.Xq8 = static_cast<int8_t*>(take((size_t)T * K));
@@ -295,7 +295,7 @@ rrs_status rrs_prepare_weights(const void* W, int32_t w_dtype, int64_t N, int64_
 // rows a1-a6 (rotate = a1 on, smooth = a2-a5 on; the variants are rrs.h RRS_NO_ROTATION / RRS_PREROTATED and the
 // RRS_NO_SMOOTH efficiency baselines)
 static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* perm, uint8_t* Xq, int8_t* Xq8,
-                           float* x_scale, float* s_group, float* chan_max, unsigned* counter, float* Xr, bool e4m3,
+                           float* x_scale, float* s_group, float* chan_max, bool want_chan_max, float* Xr, bool e4m3,
                            int group, int nsm, cudaStream_t st, bool rotate = true, bool smooth = true) {
   if (!rotate || !smooth) {  // variant prologue: two kernels
     cudaError_t e = cudaSuccess;
@@ -314,19 +314,19 @@ static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* p
                                                 e4m3, group, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_decode_kernel");
   }
-  // chan_max (and the fused kernel's CTA counter) start at zero; one memset when they are contiguous
-  const bool contiguous = reinterpret_cast<unsigned*>(chan_max) + K == counter;
-  cudaError_t e = cudaMemsetAsync(chan_max, 0, sizeof(float) * (contiguous ? K + 1 : K), st);
-  if (e == cudaSuccess && !contiguous) e = cudaMemsetAsync(counter, 0, sizeof(unsigned), st);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
-  if (T > 0 && rrs::prologue_fused_supports_k(K)) {
-    e = rrs::launch_prologue_fused(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
-                                   counter, perm, s_group, Xq, Xq8, x_scale, e4m3, group, nsm, st);
+  // prefill, K = 2^m: one cooperative launch that reduces group maxima only (s_g needs no per-channel c_j); a caller
+  // that wants chan_max, or a grid that cannot be co-resident, takes the two-kernel prologue below
+  cudaError_t e = cudaSuccess;
+  if (T > 0 && !want_chan_max && rrs::prologue_fused_supports_k(K)) {
+    e = rrs::launch_prologue_fused(static_cast<const uint16_t*>(X), T, K, Xr, perm, s_group, Xq, Xq8, x_scale, e4m3,
+                                   group, st);
     if (e == cudaSuccess) return RRS_OK;
     if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported)
-      return cuda_fail(e, "prologue_fused_kernel");
-    cudaGetLastError();  // refused (grid cannot be co-resident): the two-kernel prologue below
+      return cuda_fail(e, "prologue_group_kernel");
+    cudaGetLastError();
   }
+  e = cudaMemsetAsync(chan_max, 0, sizeof(float) * K, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(chan_max)");
   e = rrs::launch_fwht_colmax(static_cast<const uint16_t*>(X), T, K, reinterpret_cast<unsigned*>(chan_max), Xr,
                               nsm, st);
   if (e != cudaSuccess) return cuda_fail(e, "fwht_colmax_kernel");
@@ -353,9 +353,10 @@ rrs_status rrs_rotate_smooth_quant(const void* X, int32_t x_dtype, int64_t T, in
   const size_t need = carve(ws, T, 1, K, group, 0, &w);
   if (!ws || ws_bytes < need) return fail(RRS_ERR_WORKSPACE_TOO_SMALL, "need %zu workspace bytes", need);
   if (!aligned16(ws)) return fail(RRS_ERR_MISALIGNED, "workspace must be 16-byte aligned");
+  const bool want_chan_max = chan_max != nullptr;
   if (!chan_max) chan_max = w.chan_max;
-  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, reinterpret_cast<unsigned*>(w.chan_max) + K,
-                  w.Xr, (flags & RRS_OPERAND_I8) == 0, group, nsm, static_cast<cudaStream_t>(stream),
+  return prologue(X, T, K, perm, Xq, Xq8, x_scale, s_group, chan_max, want_chan_max, w.Xr,
+                  (flags & RRS_OPERAND_I8) == 0, group, nsm, static_cast<cudaStream_t>(stream),
                   (flags & (RRS_NO_ROTATION | RRS_PREROTATED)) == 0, (flags & RRS_NO_SMOOTH) == 0);
 }
 
@@ -508,9 +509,8 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
     if (T > 0)
       if (rrs_status s = gemm_checks(w.Xq8, w.x_scale, Wq8, w_scale, T, N_total, K, group, Y, ldy)) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max,
-                                reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, /*e4m3=*/false, group, nsm, st,
-                                rotate, smooth))
+    if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, false, w.Xr,
+                                /*e4m3=*/false, group, nsm, st, rotate, smooth))
       return s;
     if (T == 0) return RRS_OK;
     rrs::DecodeArgs d{w.Xq8, w.x_scale, w.s_group, Wop, w_scale, T, N_total, K, group, out_scale, Y, y_dtype, ldy};
@@ -546,8 +546,8 @@ rrs_status rrs_linear(const void* X, int32_t x_dtype, int64_t T, int64_t K, int3
         return fail(RRS_ERR_MISALIGNED, "shard width and ldy must be multiples of 16 bytes");
     }
   }
-  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max,
-                              reinterpret_cast<unsigned*>(w.chan_max) + K, w.Xr, e4m3, group, nsm, st, rotate, smooth))
+  if (rrs_status s = prologue(X, T, K, perm, nullptr, w.Xq8, w.x_scale, w.s_group, w.chan_max, false, w.Xr, e4m3,
+                              group, nsm, st, rotate, smooth))
     return s;
   if (T == 0) return RRS_OK;
   if (!comm) {

@@ -282,9 +282,10 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       }
     }
     // every MMA has completed (this warp saw the last tfull), so every converter and every ring stage of this CTA
-    // is done: the partials go to this CTA's own ring (16-byte stores, row stride TP + 4 floats), and a proxy fence
-    // makes them visible to the bulk copies below
+    // is done (the CTA barrier below states it directly as well); the partials then go to this CTA's own ring
+    // (16-byte stores, row stride TP + 4 floats) and a proxy fence makes them visible to the bulk copies
     if (warp == PROM0 && lane == 0) dtrace(7, 0);
+    asm volatile("barrier.sync 2, %0;" ::"n"(THREADS) : "memory");
     const int r = h * 128 + q * 32 + lane;
 #pragma unroll
     for (int t4 = 0; t4 < TP / 4; ++t4)
@@ -293,6 +294,8 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
             make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
     ptx::fence_proxy_async_shared();
   }
+  // the other warps' arrival at that CTA barrier (non-aligned form: producer lanes may still be diverged)
+  if (warp < PROM0 || warp >= PROM0 + NPROM) asm volatile("barrier.sync 2, %0;" ::"n"(THREADS) : "memory");
   // first cluster barrier: every CTA of the cluster is done with its ring (the peers' slots are free) and has its
   // partials in place
   ptx::tc_fence_before();
@@ -314,6 +317,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     ptx::mbar_wait(redbar, 0);  // the S - 1 incoming slices have landed
     ptx::cluster_sync_warps_arrive();  // ... so every copy out of a peer's partials has completed (joined at the end)
   }
+  __syncthreads();  // (already implied by the cluster barrier above; stated for the shared-memory race checker)
   if (threadIdx.x == 0) dtrace(7, 2);
   // ---- fixed-order reduction over the S slots (ranks 0..S-1) and the epilogue: rank r writes rows
   // [r 256/S, (r+1) 256/S) of the row block

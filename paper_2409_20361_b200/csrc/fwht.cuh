@@ -180,22 +180,26 @@ RRS_DEVICE void load_layout(const double* sm, int rr, int tp, double (&v)[P::E])
 }
 
 // The middle passes [b, HI) following a pass with layout PL; finally the H28 pass.  Ends with v in the
-// layout last_layout<P>().  Every thread of the CTA must call it.
-template <class P, int PL, int b, class Emit>
-RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, double (&v)[P::E], Emit&& emit) {
+// layout last_layout<P>().  Every thread of the CTA must call it.  `staged()` runs (in every thread) right after the
+// first CTA barrier, when every thread has consumed its pass-0 inputs (the bf16 stage may be refilled).
+template <class P, int PL, int b, class Emit, class Hook>
+RRS_DEVICE void fwht_rest(double* sm, int rr, int tp, bool p2act, bool h28act, double (&v)[P::E], Emit&& emit,
+                          Hook&& staged) {
   if constexpr (b < P::HI) {
     constexpr int r = min_c(P::B, P::HI - b);
     if (p2act) store_layout<P, PL>(sm, rr, tp, v);
     __syncthreads();
+    if constexpr (PL == -1) staged();
     if (p2act) {
       load_layout<P, b>(sm, rr, tp, v);
       butterflies<r>(v);
     }
     __syncthreads();  // the tile is rewritten by the next pass (or by the next row)
-    fwht_rest<P, b, b + r>(sm, rr, tp, p2act, h28act, v, emit);
+    fwht_rest<P, b, b + r>(sm, rr, tp, p2act, h28act, v, emit, staged);
   } else if constexpr (!P::kPow2) {
     if (p2act) store_layout<P, PL>(sm, rr, tp, v);
     __syncthreads();
+    if constexpr (PL == -1) staged();
     if (h28act) {
       load_layout<P, -2>(sm, 0, threadIdx.x, v);  // H28 layout is indexed by the CTA thread
       h28_lean(v, emit);
@@ -220,8 +224,17 @@ __host__ __device__ constexpr int last_layout() {
 // rotated value of row-local column out_col<P>(tp, j) of tile row rr (t = rr * TP2 + tp in the 2^m passes;
 // t = tp for H28).  rr and tp are set before the first emit.
 // active_rows masks rows beyond the matrix (their lanes still run, on whatever the stage holds).
-template <class P, class Emit>
-RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], int& rr, int& tp, Emit&& emit) {
+// (tile row, row-thread) of CTA thread t in the last layout: the rr / tp that fwht_tile passes to its emits
+template <class P>
+RRS_DEVICE void tile_coords(int t, int& rr, int& tp) {
+  const bool p2act = t < P::R * P::TP2;
+  rr = P::kPow2 ? (p2act ? t / P::TP2 : 0) : 0;
+  tp = P::kPow2 ? (p2act ? t % P::TP2 : 0) : t;
+}
+
+template <class P, class Emit, class Hook>
+RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], int& rr, int& tp, Emit&& emit,
+                          Hook&& staged) {
   const int t = threadIdx.x;
   const bool p2act = t < P::R * P::TP2;
   const bool h28act = !P::kPow2 && t < P::TH28;
@@ -243,13 +256,17 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], 
     }
     butterflies<P::B>(v);
   }
-  fwht_rest<P, -1, 3>(sm, rr, tp2, p2act, h28act, v, emit);
+  fwht_rest<P, -1, 3>(sm, rr, tp2, p2act, h28act, v, emit, staged);
   if constexpr (P::kPow2) {
     if (p2act) {
 #pragma unroll
       for (int j = 0; j < P::SLOTS; ++j) emit(j, __double2float_rn(v[j]));
     }
   }
+}
+template <class P, class Emit>
+RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], int& rr, int& tp, Emit&& emit) {
+  fwht_tile<P>(stage, sm, v, rr, tp, emit, [] {});
 }
 
 template <class P>

@@ -20,11 +20,11 @@
 //               = 1.95 waves of 74 pairs);
 //   warps 2-13  promotion/epilogue (lane quadrant = warp % 4, column third = (warp-2)/4: 80 columns,
 //               whose f32 accumulators stay in registers); they release a buffer on the leader's barrier.
-// Exact int32 -> f32 with no integer instruction: every accumulator buffer is pre-loaded (tcgen05.st)
-// with the bit pattern of 1.5*2^23 and the MMAs always accumulate onto it, so the buffer holds the bits
-// of the float 1.5*2^23 + P_g, exact because |P_g| <= 6272 < 2^22 (and |sum_k| <= 702464 in plain mode).
-// Promotion per pair of outputs is then one packed FADD (-1.5*2^23, exact) and one packed FFMA
-// (acc += s_g * P_g) on the f32x2 path; after reading a buffer the warp re-stores the bias and releases it.
+// int8 carrier: every accumulation starts fresh (like the FP8 carrier) and the exact int32 P_g is turned into a float
+// in registers with the magic-number trick -- bits(P + 0x4B400000) is the float 1.5*2^23 + P, exact because
+// |P| <= 6272 < 2^22 (|sum_k| <= 702464 in plain mode), and one packed FADD of -1.5*2^23 leaves P -- one integer
+// add on the ALU pipe per output instead of re-arming TMEM with a bias after every group (which needed a
+// cluster-scope release per group and ran the C3-up GEMM at 2.2x the FP8 carrier's time, bench r2s).
 // The MMA of group g+1 overlaps the promotion of group g (two TMEM buffers).  In plain mode (the
 // per-channel A4W4 baseline of P:322) the MMA accumulates all K into one buffer per tile instead.
 #include <algorithm>
@@ -144,8 +144,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
   float* s_sm = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 1024);
   float* beta_sm = s_sm + MAX_G;     // [2][BN]   beta of the current tile (double-buffered by tile parity)
   float* xs_sm = beta_sm + 2 * BN;   // [2][BM]   alpha_t of the current / next tile's rows
-  uint32_t* bias_sm = reinterpret_cast<uint32_t*>(xs_sm + 2 * BM);  // [8] = 0x4B400000
-  float* bsub_sm = reinterpret_cast<float*>(bias_sm + 16);            // [3][BN] sub-channel beta_g ring
+  float* bsub_sm = xs_sm + 2 * BM + 16;  // [3][BN] sub-channel beta_g ring
 
   const uint32_t warp = ptx::warp_idx();
   const int lane = threadIdx.x & 31;
@@ -170,7 +169,6 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     if constexpr (kCta == 2) ptx::tmem_alloc2(taddr_slot, 512);
     else ptx::tmem_alloc(taddr_slot, 512);
   }
-  if (threadIdx.x < 8) bias_sm[threadIdx.x] = 0x4B400000u;
   if constexpr (kCta == 2) ptx::cluster_sync();  // peer barriers initialised before any remote arrive / TMA
   ptx::pdl_wait();  // Xq8 / x_scale / s_group come from the prologue kernels (programmatic dependent launch)
   if (!kPlain && p.s_group) {
@@ -222,8 +220,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     auto wait_tempty = [&](uint32_t b) {
       // a new accumulation into buffer b: use u = acc_iter >> 1 of it needs the u-th release (completion #u
       // of tempty[b]); the releases come from both CTAs of a pair (cluster-scope acquire for int8)
-      if constexpr (kCta == 2 && !kFp8) ptx::mbar_wait_cluster(&tempty[b], (acc_iter >> 1) & 1);
-      else if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
+      if constexpr (RRS_GEMM_SPIN_MMA) ptx::mbar_wait_spin(&tempty[b], (acc_iter >> 1) & 1);
       else ptx::mbar_wait(&tempty[b], (acc_iter >> 1) & 1);
     };
     auto wait_full = [&]() {
@@ -232,14 +229,13 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       ptx::tc_fence_after();
     };
     auto mma = [&](uint32_t d, uint64_t a_desc, uint64_t b_desc, int k, uint32_t acc) {
-      // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row.  int8 carrier: always
-      // accumulate (the buffer starts at the magic bias); FP8 carrier: a fresh sum per group.
+      // advance 32 bytes (= 32 one-byte codes) along K inside the 128-byte swizzle row; a fresh sum per group
       if constexpr (kFp8) {
         if constexpr (kCta == 1) ptx::mma_f8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
         else ptx::mma_f8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
       } else {
-        if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
-        else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, 1u);
+        if constexpr (kCta == 1) ptx::mma_i8(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
+        else ptx::mma_i8_pair(d, a_desc + 2 * k, b_desc + 2 * k, idesc, acc);
       }
     };
     auto commit = [&](uint64_t* bar) {
@@ -312,15 +308,6 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
     const int half = ew >> 2;                // column quarter of the 256-wide tile
     const int row_in_tile = quad * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
-    // int8 carrier: bias both accumulator buffers once (completion #0 of tempty[0] and tempty[1])
-    if constexpr (!kFp8) {
-#pragma unroll
-      for (int b = 0; b < 2; ++b)
-#pragma unroll
-        for (int cc = 0; cc < EPI_COLS / 16; ++cc)
-          RRS_TMEM_ST16_SPLAT(tmem_base + lane_off + b * ACC_STRIDE + half * EPI_COLS + cc * 16, kBias);
-      ptx::tmem_st_wait();
-    }
     ptx::tc_fence_before();
     __syncwarp();
     // buffer releases go to the pair leader's tempty barriers
@@ -337,18 +324,12 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
       __syncwarp();
       if (lane == 0) {
 #endif
-        if constexpr (kFp8) ptx::mbar_arrive_remote(addr);
-        else ptx::mbar_arrive_cluster(addr);  // release at cluster scope: orders the bias re-arm tcgen05.st
+        ptx::mbar_arrive_remote(addr);
       }
     };
     release(tempty_addr0);
     release(tempty_addr1);
     const float2 neg_bias2 = make_float2(-12582912.0f, -12582912.0f);  // -1.5*2^23
-    // eight registers holding the bias bits, the source of the re-arming tcgen05.st (kept live across the
-    // loop; their value comes from shared memory so it is not re-materialised as an immediate)
-    uint32_t bias8[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) bias8[j] = bias_sm[j];
     uint32_t acc_iter = 0;
     int it = 0;  // local tile counter
     const int tile_stride = gridDim.x / kCta;
@@ -461,7 +442,7 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
                   s23, make_float2(__uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])), acc2[cc * 8 + 2 * q + 1]);
             }
           }
-        } else if constexpr (kFp8 && !kDebug) {
+        } else if constexpr (!kDebug) {
           // software-pipelined: chunk c+1 is in flight while chunk c is accumulated; the buffer is released
           // as soon as the last chunk has landed in registers
           constexpr int NCH = EPI_COLS / 16;
@@ -478,9 +459,13 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             if (false)
 #endif
 #pragma unroll
-            for (int j = 0; j < 8; ++j)  // acc += s_g * P_g (R14); the FP8 carrier's P_g is an exact float
-              acc2[cc * 8 + j] = __ffma2_rn(s2, make_float2(__uint_as_float(cur[2 * j]), __uint_as_float(cur[2 * j + 1])),
-                                            acc2[cc * 8 + j]);
+            for (int j = 0; j < 8; ++j) {  // acc += s_g * P_g (R14); the FP8 carrier's P_g is an exact float
+              float2 f = make_float2(__uint_as_float(cur[2 * j]), __uint_as_float(cur[2 * j + 1]));
+              if constexpr (!kFp8)  // int8: bits(P + 0x4B400000) - 1.5*2^23 = P exactly (|P| < 2^22)
+                f = __fadd2_rn(make_float2(__uint_as_float(cur[2 * j] + kBias), __uint_as_float(cur[2 * j + 1] + kBias)),
+                               neg_bias2);
+              acc2[cc * 8 + j] = __ffma2_rn(s2, f, acc2[cc * 8 + j]);
+            }
             if (cc + 1 < NCH) {
               RRS_TMEM_WAIT_LD16(nxt);
               if (cc + 2 == NCH) {  // all chunks of this buffer are in registers: release it
@@ -495,36 +480,30 @@ rrs_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constan
             uint32_t r[16];
             RRS_TMEM_LD16(tbase + cc * 16, r);
             RRS_TMEM_WAIT_LD16(r);
-            if constexpr (kFp8) {
-              if (cc == EPI_COLS / 16 - 1) {
-                // every column of this buffer is in registers: release it before the last chunk's math
-                release(b ? tempty_addr1 : tempty_addr0);
-              }
+            if (cc == EPI_COLS / 16 - 1) {
+              // every column of this buffer is in registers: release it before the last chunk's math
+              release(b ? tempty_addr1 : tempty_addr0);
             }
             if (kDebug && row < p.T) {
               const int gg = kPlain ? 0 : g;
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const int n = col0 + cc * 16 + j;
-                const int32_t P = kFp8 ? __float2int_rn(__uint_as_float(r[j])) : (int32_t)(r[j] - kBias);
+                const int32_t P = kFp8 ? __float2int_rn(__uint_as_float(r[j])) : (int32_t)r[j];
                 if (n < p.N) p.P_debug[((int64_t)gg * p.T + row) * p.N + n] = P;
               }
             }
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               float2 f = make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
-              // int8 carrier: (1.5*2^23 + P) - 1.5*2^23 = P exactly for |P| < 2^22; FP8 carrier: P is already
-              // an exact float.  Then acc += s_g * P (R14).
-              if constexpr (!kFp8) f = __fadd2_rn(f, neg_bias2);
+              // int8 carrier: bits(P + 0x4B400000) = 1.5*2^23 + P, minus 1.5*2^23 = P exactly for |P| < 2^22; FP8
+              // carrier: P is already an exact float.  Then acc += s_g * P (R14).
+              if constexpr (!kFp8)
+                f = __fadd2_rn(make_float2(__uint_as_float(r[2 * j] + kBias), __uint_as_float(r[2 * j + 1] + kBias)),
+                               neg_bias2);
               acc2[cc * 8 + j] = __ffma2_rn(s2, f, acc2[cc * 8 + j]);
             }
           }
-        }
-        if constexpr (!kFp8) {
-#pragma unroll
-          for (int cc = 0; cc < EPI_COLS / 8; ++cc) RRS_TMEM_ST8(tbase + cc * 8, bias8);  // re-arm
-          ptx::tmem_st_wait();
-          release(b ? tempty_addr1 : tempty_addr0);
         }
         ++acc_iter;
       }

@@ -44,12 +44,12 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), int grid, int threads, int smem, 
 bool prologue_supports_k(int64_t K);
 cudaError_t launch_fwht_colmax(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
                                int nsm, cudaStream_t st);
-// One persistent (cooperative) launch of rows a1-a6 for K = 2^m; chan_max and *counter must be zero on entry.
-// Returns cudaErrorCooperativeLaunchTooLarge (error state cleared) when the grid cannot be co-resident.
+// One persistent (cooperative) launch of rows a1-a6 for K = 2^m that reduces group maxima only (no chan_max output;
+// no zeroed input).  Returns cudaErrorCooperativeLaunchTooLarge when the grid cannot be co-resident.
 bool prologue_fused_supports_k(int64_t K);
-cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
-                                  unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                  float* scale, bool e4m3, int group, int nsm, cudaStream_t st);
+cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, float* Xr, const int32_t* perm,
+                                  float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int group,
+                                  cudaStream_t st);
 // Decode-sized T (1..64, K = 2^m in [1024, 8192]): rows a1-a6 in one cooperative launch, one CTA per row, the FWHT
 // of a row spread over its K/1024 warps; no memset (chan_max is written, not accumulated).  scratch: >= T * K f32.
 bool prologue_decode_supports(int64_t T, int64_t K, int group);

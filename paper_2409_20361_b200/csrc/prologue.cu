@@ -11,6 +11,7 @@
 //                         (W is permuted, never scaled).
 //   perm_rank_kernel    : offline reorder helper (R5): perm = argsort(c) descending, ties ascending.
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 
 #include "fwht.cuh"
@@ -91,19 +92,16 @@ RRS_DEVICE void fwht_phase(const uint16_t* __restrict__ X, int64_t T, unsigned* 
     trace(0, 1 + 2 * (it < 5 ? it : 5));
     double v[P::E];
     int rr = 0, tp = 0;
-    float* xr = nullptr;
-    bool live = false;
-    // X~ stores and column maxima as the values are produced (rr / tp are set before the first call)
+    // X~ stores and column maxima as the values are produced; the row and its pointer are fixed before the
+    // transform, so every store is one base register plus a compile-time offset and nothing branches per element
+    int rr0, tp0;
+    tile_coords<P>((int)threadIdx.x, rr0, tp0);
+    const int64_t row = tile * P::R + rr0;
+    const bool live = act && row < T;
+    float* xr = Xr + (live ? row : 0) * (int64_t)K;
     auto emit = [&](int j, float f) {
-      if (!xr) {
-        const int64_t row = tile * P::R + rr;
-        live = row < T;
-        xr = Xr + row * K;
-      }
-      if (live) {
-        cm[j] = fmaxf(cm[j], fabsf(f));
-        xr[out_col<P>(tp, j)] = f;
-      }
+      cm[j] = live ? fmaxf(cm[j], fabsf(f)) : cm[j];
+      if (live) xr[out_col<P>(tp0, j)] = f;
     };
     fwht_tile<P>(stage + buf * P::TILE, sm, v, rr, tp, emit);  // ends with __syncthreads: stage[buf] is free
     trace(0, 2 + 2 * (it < 5 ? it : 5));
@@ -211,38 +209,11 @@ RRS_DEVICE float group_inv_scale(const float* cms, const int (&pj)[32], int j0, 
   return __frcp_rn(m);
 }
 
-// Quantise this thread's 32 positions of one row held in shared memory (xs = the row's f32 values in natural
-// column order): Z = X~[perm] * inv_s (Eq. 2 P:91, R9), per-token absmax over the TPR threads of the row,
-// alpha = fl(m/7), codes rint_even(fl(Z * fl(7/m))) clamped to [-8, 7] (P:48, R9-R11), packed nibbles and
-// operand bytes.  Contains __syncthreads() when TPR > 32 (every thread of the CTA must call it);
-// `after_reads` runs once every thread has finished reading xs (the caller recycles the buffer there).
-template <int TPR, class F>
-RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, bool smooth, float* red, int tid, int rr,
-                          int64_t trow, int64_t T, int K, int j0, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
-                          float* __restrict__ scale_out, bool e4m3, F after_reads, bool dec4 = false) {
-  float z[32];
-  float m = 0.0f;
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const float x = xs[pj[k]];
-    z[k] = smooth ? __fmul_rn(x, inv_s) : x;
-    m = fmaxf(m, fabsf(z[k]));
-  }
-  if constexpr (TPR <= 32) {
-    m = seg_max(m, TPR);
-  } else {
-    m = seg_max(m, 32);
-    if ((tid & 31) == 0) red[tid >> 5] = m;
-    __syncthreads();
-    const int w0 = (rr * TPR) >> 5;
-    float mm = 0.0f;
-#pragma unroll 4
-    for (int w = 0; w < TPR / 32; ++w) mm = fmaxf(mm, red[w0 + w]);
-    m = mm;
-  }
-  __syncthreads();  // every thread has read xs (and red): both may be reused
-  after_reads();
-  if (trow >= T) return;
+// Codes of this thread's 32 smoothed values z (positions j0..j0+31 of row trow) given the row's absmax m: alpha =
+// fl(m/7), codes rint_even(fl(z * fl(7/m))) clamped to [-8, 7] (R9-R11), packed nibbles (D4 or the decode4
+// tiled layout) and / or the GEMM operand bytes; the j0 == 0 thread stores alpha.
+RRS_DEVICE void write_codes(const float (&z)[32], float m, int64_t trow, int K, int j0, uint8_t* __restrict__ Xq,
+                            int8_t* __restrict__ Xq8, float* __restrict__ scale_out, bool e4m3, bool dec4) {
   float alpha = 1.0f, r = 0.0f;
   if (m > 0.0f) {
     alpha = __fdiv_rn(m, 7.0f);  // stored scale alpha_t = fl(m/7)
@@ -304,83 +275,230 @@ RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, boo
   if (j0 == 0) scale_out[trow] = alpha;
 }
 
-// Fused runtime prologue for K = 2^m (rows a1-a6 in one persistent launch): the FWHT pass above, a grid-wide
-// barrier (the grid is sized to be co-resident: max active clusters), then the quantisation pass on the same
-// CTAs and the same rows (their X~ is still in L2).  `counter` (next to chan_max, zeroed with it) counts CTAs.
+// Quantise this thread's 32 positions of one row held in shared memory (xs = the row's f32 values in natural
+// column order): Z = X~[perm] * inv_s (Eq. 2 P:91, R9), per-token absmax over the TPR threads of the row,
+// alpha = fl(m/7), codes rint_even(fl(Z * fl(7/m))) clamped to [-8, 7] (P:48, R9-R11), packed nibbles and
+// operand bytes.  Contains __syncthreads() when TPR > 32 (every thread of the CTA must call it);
+// `after_reads` runs once every thread has finished reading xs (the caller recycles the buffer there).
+template <int TPR, class F>
+RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, bool smooth, float* red, int tid, int rr,
+                          int64_t trow, int64_t T, int K, int j0, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
+                          float* __restrict__ scale_out, bool e4m3, F after_reads, bool dec4 = false) {
+  float z[32];
+  float m = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const float x = xs[pj[k]];
+    z[k] = smooth ? __fmul_rn(x, inv_s) : x;
+    m = fmaxf(m, fabsf(z[k]));
+  }
+  if constexpr (TPR <= 32) {
+    m = seg_max(m, TPR);
+  } else {
+    m = seg_max(m, 32);
+    if ((tid & 31) == 0) red[tid >> 5] = m;
+    __syncthreads();
+    const int w0 = (rr * TPR) >> 5;
+    float mm = 0.0f;
+#pragma unroll 4
+    for (int w = 0; w < TPR / 32; ++w) mm = fmaxf(mm, red[w0 + w]);
+    m = mm;
+  }
+  __syncthreads();  // every thread has read xs (and red): both may be reused
+  after_reads();
+  if (trow >= T) return;
+  write_codes(z, m, trow, K, j0, Xq, Xq8, scale_out, e4m3, dec4);
+}
+
+// ------------------------------------------------------------------------------ a1-a6 fused (prefill, K = 2^m)
+//
+// One cooperative launch for the whole prologue.  Only s_g reaches the GEMM, and s_g = max over j' in g of
+// c_{perm[j']} = max over (t, j' in g) of |X~_{t, perm[j']}| (Eq. 1-2 P:90-91 with the reorder P:106): a max over
+// tokens and the group's channels jointly, so this kernel never forms the per-channel c_j (calls that want chan_max
+// take the two-kernel path, api.cu):
+//   pass 1, per tile of R rows: FWHT (fwht.cuh) -> X~ rounded once to f32 into shared memory (natural column
+//     order, over the idle transpose tile) -> each thread gathers its chunk of 32 reordered positions j0..j0+31
+//     (perm, through a table of 16-bit shared-memory byte offsets built once per CTA), folds max |X~| into one
+//     running maximum (32 | group, so the chunk lies in one group) and stores the 32 values to the workspace in a
+//     layout private to this kernel: row t, float4 q < 8 of chunk c at Xr[t K + 4 (q K/32 + c)] (a warp's 16-byte
+//     stores are contiguous);
+//   group maxima: shared-memory atomicMax per CTA, then one red.max per group per CTA into gmax[G] (library memory);
+//   grid barrier (one thread per cluster arrives; the launch is cooperative, so every CTA is resident);
+//   pass 2, the same tiles on the same threads (the values are still in L2): s_g (0 -> 1, R8), Z = X~ * fl(1/s_g)
+//     (R9), per-token absmax over the row's K/32 threads, codes (write_codes).
+// gmax and the barrier counters live in library memory, one slot per call (concurrent calls use different slots),
+// zero at module load and reset by the last CTA to leave: no memset launch precedes this kernel.
+constexpr int kGroupSlots = 256;
+constexpr int kMaxG = 160;  // api.cu kMaxGroups
+__device__ unsigned g_group_gmax[kGroupSlots][kMaxG];
+__device__ unsigned g_group_bar[kGroupSlots][2];  // [arrive (clusters), depart (CTAs)]
+
+template <int K>
+struct GroupSmem {
+  using P = FwhtPlan<K>;
+  static constexpr int TPQ = K / 32;                                      // gather chunks per row
+  static constexpr int TILE_D = ((P::TILE_PAD * 8 + 127) / 128) * 128;  // fp64 transposes, then the f32 X~ tile
+  static constexpr int STAGE = P::TILE * 2;                             // the bf16 tile (single buffer)
+  static constexpr int TBL = P::TILE * 2;                               // 32 u16 offsets per thread
+  static constexpr int BYTES = TILE_D + STAGE + TBL + kMaxG * 4 + 2 * 32 * 4 + 16;  // + gmax, red[2][32], barrier
+  static_assert(P::kPow2 && P::E == 32 && P::THREADS == P::R * TPQ, "one gather chunk per thread per tile row");
+  static_assert(P::TILE * 4 <= TILE_D && P::TILE * 4 <= 65536, "f32 X~ tile overlays the transposes; u16 offsets");
+};
+
 template <int K>
 __global__ void __cluster_dims__(colmax_cluster<K>(), 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
-prologue_fused_kernel(const uint16_t* __restrict__ X, int64_t T, unsigned* __restrict__ chan_max_bits,
-                      float* __restrict__ Xr, unsigned* __restrict__ counter, const int32_t* __restrict__ perm,
-                      float* __restrict__ s_group_out, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
-                      float* __restrict__ scale_out, int e4m3, int group) {
+prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restrict__ Xr,
+                      const int32_t* __restrict__ perm, float* __restrict__ s_group_out, uint8_t* __restrict__ Xq,
+                      int8_t* __restrict__ Xq8, float* __restrict__ scale_out, int e4m3, int group, unsigned slot) {
   using P = FwhtPlan<K>;
-  using S = ColmaxSmem<K>;
-  static_assert(P::kPow2 && P::E == 32, "fused prologue: 2^m plans (32 positions per thread in both passes)");
-  constexpr int TPR = K / 32;  // quantisation threads per row == FWHT threads per row
+  using S = GroupSmem<K>;
+  constexpr int TPQ = S::TPQ;
   extern __shared__ __align__(128) uint8_t smem[];
-  fwht_phase<K, false>(X, T, chan_max_bits, Xr, smem);
+  double* sm = reinterpret_cast<double*>(smem);
+  float* xs = reinterpret_cast<float*>(smem);  // the f32 X~ tile [R][K], natural order (after the FWHT)
+  uint16_t* stage = reinterpret_cast<uint16_t*>(smem + S::TILE_D);
+  uint4* tbl = reinterpret_cast<uint4*>(smem + S::TILE_D + S::STAGE);  // [4][THREADS] uint4 = 8 u16 offsets each
+  unsigned* gmax_sm = reinterpret_cast<unsigned*>(smem + S::TILE_D + S::STAGE + S::TBL);
+  float* red = reinterpret_cast<float*>(gmax_sm + kMaxG);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * 32);
+  unsigned* gmax = g_group_gmax[slot];
+  unsigned* gbar = g_group_bar[slot];
   const int tid = threadIdx.x;
-  const int rr = tid / TPR, j0 = (tid % TPR) * 32;
-  int pj[32];
-  load_perm32(perm, j0, pj);  // an offline input: these loads overlap the grid barrier
+  const int rr = tid / TPQ, c = tid % TPQ, j0 = c * 32;  // this thread's gather chunk: row rr of a tile, j0..j0+31
+  const int G = K / group;
+  const int64_t ntiles = (T + P::R - 1) / P::R;
 
-  // ---- grid barrier (X~ stores -- read back below by TMA, i.e. the async proxy -- and chan_max atomics
-  // visible everywhere): every thread fences, the cluster synchronises, one thread per cluster counts in
-  // and waits for all clusters, then releases its cluster
-  trace(1, 0);
+  auto issue = [&](int64_t tile) {
+    const int64_t rows = (T - tile * P::R) < P::R ? (T - tile * P::R) : P::R;
+    const uint32_t bytes = (uint32_t)(rows * K * 2);
+    ptx::mbar_arrive_expect_tx(bar, bytes);
+    ptx::bulk_load(stage, X + tile * P::R * K, bytes, bar);
+  };
+  if (tid == 0) {
+    ptx::mbar_init(bar, 1);
+    ptx::fence_barrier_init();
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
+  {  // gather table: byte offset in xs of (row rr, column perm[j0 + k]), two per word (an offline input)
+    const int4* pp = reinterpret_cast<const int4*>(perm + j0);
+    uint32_t w[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int4 p4 = __ldg(pp + q);
+      w[2 * q] = (uint32_t)((rr * K + p4.x) * 4) | ((uint32_t)((rr * K + p4.y) * 4) << 16);
+      w[2 * q + 1] = (uint32_t)((rr * K + p4.z) * 4) | ((uint32_t)((rr * K + p4.w) * 4) << 16);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tbl[q * P::THREADS + tid] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
+    for (int g = tid; g < kMaxG; g += P::THREADS) gmax_sm[g] = 0u;
+  }
+  // (the table and gmax_sm are first read after the FWHT's barriers)
+
+  // ---- pass 1
+  float gm = 0.0f;
+  int rf, tf;  // (tile row, row-thread) of this thread in the FWHT's last layout
+  tile_coords<P>(tid, rf, tf);
+  float* xs_row = xs + rf * K;
+  int it = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    ptx::mbar_wait(bar, it & 1);
+    double v[P::E];
+    int rr_, tp_;
+    fwht_tile<P>(stage, sm, v, rr_, tp_, [&](int j, float f) { xs_row[out_col<P>(tf, j)] = f; },
+                 [&] { if (tid == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x); });
+    __syncthreads();  // the X~ tile is complete
+    float z[32];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint4 o = tbl[q * P::THREADS + tid];
+      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        z[8 * q + 2 * h] = *reinterpret_cast<const float*>(smem + (ow[h] & 0xFFFFu));
+        z[8 * q + 2 * h + 1] = *reinterpret_cast<const float*>(smem + (ow[h] >> 16));
+      }
+    }
+    __syncthreads();  // every gather is done: the tile is rewritten by the next FWHT
+    const int64_t trow = tile * P::R + rr;
+    if (trow < T) {
+      float4* dst = reinterpret_cast<float4*>(Xr + trow * K) + c;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        gm = fmaxf(gm, fmaxf(fmaxf(fabsf(z[4 * q]), fabsf(z[4 * q + 1])), fmaxf(fabsf(z[4 * q + 2]), fabsf(z[4 * q + 3]))));
+        dst[q * TPQ] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
+      }
+    }
+  }
+  // ---- group maxima (values >= +0: unsigned order of the float bits is the float order)
+  atomicMax(gmax_sm + j0 / group, __float_as_uint(gm));
+  __syncthreads();
+  for (int g = tid; g < G; g += P::THREADS)
+    if (gmax_sm[g]) atomicMax(gmax + g, gmax_sm[g]);
+
+  // ---- grid barrier: the Xr stores and the gmax atomics are visible everywhere
   __threadfence();
-  asm volatile("fence.proxy.async.global;" ::: "memory");
   ptx::cluster_sync();
-  if (ptx::cluster_ctarank() == 0 && threadIdx.x == 0) {
-    atomicAdd(counter, 1u);
+  if (ptx::cluster_ctarank() == 0 && tid == 0) {
+    __threadfence();  // (cumulative: orders the whole cluster's stores and atomics before the arrival)
+    atomicAdd(&gbar[0], 1u);
     const unsigned nclusters = gridDim.x / colmax_cluster<K>();
     unsigned v;
-    for (;;) {  // plain spin (one thread per cluster): __nanosleep here cost ~2 us of wake-up latency (trace r2c)
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&gbar[0]) : "memory");
       if (v >= nclusters) break;
     }
   }
   ptx::cluster_sync();
-  trace(1, 1);
 
-  // ---- quantisation pass (a3-a6) on this CTA's rows
-  float* stage = reinterpret_cast<float*>(smem);                                   // 2 f32 row tiles
-  float* cms = reinterpret_cast<float*>(smem + S::TILE_D);                         // chan_max [K]
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + S::TILE_D + 2 * S::STAGE) + 2;  // 3 fresh barriers
-  float* red = reinterpret_cast<float*>(smem + S::TILE_D + 2 * S::STAGE + 64);
-  const int64_t ntiles = (T + P::R - 1) / P::R;
-  auto issue = [&](int64_t tile, int buf) {
-    const int64_t rows = (T - tile * P::R) < P::R ? (T - tile * P::R) : P::R;
-    const uint32_t bytes = (uint32_t)(rows * K * 4);
-    ptx::mbar_arrive_expect_tx(&bar[buf], bytes);
-    ptx::bulk_load(stage + buf * P::TILE, Xr + tile * P::R * K, bytes, &bar[buf]);
-  };
-  if (tid == 0) {
-    // chan_max -> every CTA of the cluster: each rank fetches one eighth once from L2 and multicasts it
-    ptx::mbar_arrive_expect_tx(&bar[2], K * 4);
-    const uint32_t rank = ptx::cluster_ctarank();
-    constexpr int SL = K / colmax_cluster<K>();
-    ptx::bulk_load_multicast(cms + rank * SL, chan_max_bits + rank * SL, SL * 4, &bar[2],
-                             (uint16_t)((1u << colmax_cluster<K>()) - 1));
-    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
-    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+  // ---- pass 2
+  for (int g = tid; g < G; g += P::THREADS) {
+    float s = __uint_as_float(__ldcg(gmax + g));
+    s = s == 0.0f ? 1.0f : s;  // R8
+    reinterpret_cast<float*>(gmax_sm)[g] = s;
+    if (blockIdx.x == 0) s_group_out[g] = s;
   }
-  trace(1, 2);
-  ptx::mbar_wait(&bar[2], 0);
-  trace(1, 4);
-  const float inv_s = group_inv_scale(cms, pj, j0, blockIdx.x == 0 && rr == 0, s_group_out, group);
-  trace(1, 5);
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int buf = it & 1;
-    ptx::mbar_wait(&bar[buf], (it >> 1) & 1);  // bar[0], bar[1] of this pass (fresh: phase 0 first)
-    trace(1, 6 + (it < 8 ? it : 8));
-    quant_row<TPR>(stage + buf * P::TILE + rr * K, pj, inv_s, true, red, tid, rr, tile * P::R + rr, T, K, j0, Xq, Xq8,
-                   scale_out, e4m3 != 0, [&] {
-                     if (tid == 0 && tile + 2 * (int64_t)gridDim.x < ntiles) issue(tile + 2 * (int64_t)gridDim.x, buf);
-                   });
+  __syncthreads();
+  const float inv_s = __frcp_rn(reinterpret_cast<const float*>(gmax_sm)[j0 / group]);  // R9
+  if (tid == 0) {  // this CTA has read gmax: the last CTA out resets the slot for a later call
+    __threadfence();
+    if (atomicAdd(&gbar[1], 1u) == gridDim.x - 1) {
+      for (int g = 0; g < G; ++g) gmax[g] = 0u;
+      gbar[0] = 0u;
+      gbar[1] = 0u;
+    }
   }
-  trace(1, 15);
+  int pr = 0;
+  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, pr ^= 1) {
+    const int64_t trow = tile * P::R + rr;
+    const bool live = trow < T;
+    float z[32];
+    float m = 0.0f;
+    const float4* src = reinterpret_cast<const float4*>(Xr + (live ? trow : 0) * K) + c;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 x = live ? __ldcg(src + q * TPQ) : make_float4(0.f, 0.f, 0.f, 0.f);
+      z[4 * q] = __fmul_rn(x.x, inv_s);
+      z[4 * q + 1] = __fmul_rn(x.y, inv_s);
+      z[4 * q + 2] = __fmul_rn(x.z, inv_s);
+      z[4 * q + 3] = __fmul_rn(x.w, inv_s);
+      m = fmaxf(m, fmaxf(fmaxf(fabsf(z[4 * q]), fabsf(z[4 * q + 1])), fmaxf(fabsf(z[4 * q + 2]), fabsf(z[4 * q + 3]))));
+    }
+    if constexpr (TPQ <= 32) {
+      m = seg_max(m, TPQ);
+    } else {  // the row's TPQ / 32 warps through red[pr] (double-buffered: one barrier per tile)
+      m = seg_max(m, 32);
+      float* rb = red + pr * 32;
+      if ((tid & 31) == 0) rb[tid >> 5] = m;
+      __syncthreads();
+      const int w0 = (rr * TPQ) >> 5;
+      float mm = 0.0f;
+#pragma unroll 4
+      for (int w = 0; w < TPQ / 32; ++w) mm = fmaxf(mm, rb[w0 + w]);
+      m = mm;
+    }
+    if (live) write_codes(z, m, trow, K, j0, Xq, Xq8, scale_out, e4m3 != 0, false);
+  }
   ptx::pdl_launch_dependents();
 }
 
@@ -733,7 +851,11 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
   const int64_t ntiles = (T + Q::R - 1) / Q::R;
   const bool smooth = chan_max_bits != nullptr;
 
-  auto issue = [&](int64_t tile, int buf) {
+  // tiles are visited in REVERSE order: the rotate pass wrote the highest rows last, so when X~ is larger than L2
+  // (C3 down: 235 MB) its most recently written part is still in L2 when this pass starts
+  auto phys = [&](int64_t li) { return ntiles - 1 - li; };
+  auto issue = [&](int64_t li, int buf) {
+    const int64_t tile = phys(li);
     const int64_t rows = (T - tile * Q::R) < Q::R ? (T - tile * Q::R) : Q::R;
     const uint32_t bytes = (uint32_t)(rows * K * 4);
     ptx::mbar_arrive_expect_tx(&bar[buf], bytes);
@@ -771,7 +893,7 @@ smooth_quant_kernel(const float* __restrict__ Xr, int64_t T, const int32_t* __re
     const int buf = it % STAGES;
     ptx::mbar_wait(&bar[buf], (it / STAGES) & 1);
     trace(1, 3 + (it < 10 ? it : 10));
-    quant_row<TPR>(stage + buf * Q::TILE + rr * K, pj, inv_s, smooth, red, tid, rr, tile * Q::R + rr, T, K, j0, Xq,
+    quant_row<TPR>(stage + buf * Q::TILE + rr * K, pj, inv_s, smooth, red, tid, rr, phys(tile) * Q::R + rr, T, K, j0, Xq,
                    Xq8, scale_out, e4m3 != 0, [&] {
                      if (tid == 0 && tile + STAGES * (int64_t)gridDim.x < ntiles)
                        issue(tile + STAGES * (int64_t)gridDim.x, buf);
@@ -827,24 +949,24 @@ static cudaError_t launch_colmax_k(const uint16_t* X, int64_t T, unsigned* cm, f
 }
 
 template <int K>
-static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, float* Xr, unsigned* counter,
-                                  const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3,
-                                  int group, int nsm, cudaStream_t st) {
+static cudaError_t launch_group_k(const uint16_t* X, int64_t T, float* Xr, const int32_t* perm, float* s_group,
+                                  uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int group, unsigned slot,
+                                  cudaStream_t st) {
   using P = FwhtPlan<K>;
-  auto kern = prologue_fused_kernel<K>;
-  const int smem = ColmaxSmem<K>::BYTES;
+  auto kern = prologue_group_kernel<K>;
+  const int smem = GroupSmem<K>::BYTES;
   cudaError_t e = prepare_kernel(kern, smem, P::THREADS);
   if (e != cudaSuccess) return e;
-  // every CTA must be resident at once (grid barrier): the grid is at most the co-resident cluster count, and
-  // the launch is COOPERATIVE, so the runtime refuses it (instead of letting it hang) when the grid cannot be
-  // co-resident; the caller then falls back to the two-kernel prologue
+  // every CTA must be resident at once (grid barrier): the grid is at most the co-resident cluster count, and the
+  // launch is COOPERATIVE, so the runtime refuses it (instead of letting it hang) when the grid cannot be co-resident;
+  // the caller then falls back to the two-kernel prologue
   const int max_clusters = max_active_clusters(kern, colmax_cluster<K>(), P::THREADS, smem);
   if (max_clusters < 1) return cudaErrorCooperativeLaunchTooLarge;
   const int64_t tiles = (T + P::R - 1) / P::R;
-  const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>()));
-  const int grid = (int)clusters * colmax_cluster<K>();
+  const int64_t clusters =
+      std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>()));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
+  cfg.gridDim = dim3((unsigned)(clusters * colmax_cluster<K>()));
   cfg.blockDim = dim3(P::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -853,7 +975,7 @@ static cudaError_t launch_fused_k(const uint16_t* X, int64_t T, unsigned* cm, fl
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, X, T, cm, Xr, counter, perm, s_group, Xq, Xq8, scale, (int)e4m3, group);
+  return cudaLaunchKernelEx(&cfg, kern, X, T, Xr, perm, s_group, Xq, Xq8, scale, (int)e4m3, group, slot);
 }
 
 template <int K>
@@ -880,11 +1002,14 @@ static cudaError_t launch_quant_k(const float* Xr, int64_t T, const int32_t* per
 
 bool prologue_fused_supports_k(int64_t K) { return K >= 128 && K <= 16384 && (K & (K - 1)) == 0; }
 
-cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, unsigned* chan_max_bits, float* Xr,
-                                  unsigned* counter, const int32_t* perm, float* s_group, uint8_t* Xq, int8_t* Xq8,
-                                  float* scale, bool e4m3, int group, int nsm, cudaStream_t st) {
+cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, float* Xr, const int32_t* perm,
+                                  float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int group,
+                                  cudaStream_t st) {
+  if (K / group > kMaxG) return cudaErrorInvalidValue;
+  static std::atomic<unsigned> calls{0};  // gmax / barrier slot per call: concurrent calls use different slots
+  const unsigned slot = calls.fetch_add(1u, std::memory_order_relaxed) % kGroupSlots;
   switch (K) {
-#define RRS_CASE(k) case k: return launch_fused_k<k>(X, T, chan_max_bits, Xr, counter, perm, s_group, Xq, Xq8, scale, e4m3, group, nsm, st);
+#define RRS_CASE(k) case k: return launch_group_k<k>(X, T, Xr, perm, s_group, Xq, Xq8, scale, e4m3, group, slot, st);
     RRS_FOR_EACH_POW2_K(RRS_CASE)
 #undef RRS_CASE
     default: return cudaErrorInvalidValue;

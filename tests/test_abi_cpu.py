@@ -53,7 +53,7 @@ def test_host_only_calls_work_without_gpu(lib_path):
     assert l.rrs_status_str(2) == b"RRS_ERR_UNSUPPORTED_SHAPE"
     # workspace sizing: X~ f32 + chan_max + s_group + x_scale + Xq8, 256-byte aligned
     ws = rrs.rrs_workspace_bytes(2048, 4096, 4096, 128, 1)
-    assert ws == 2048 * 4096 * 4 + (4096 + 64) * 4 + 256 + 8192 + 2048 * 4096
+    assert ws == 2048 * 4096 * 4 + 4096 * 4 + 256 + 8192 + 2048 * 4096
     assert rrs.rrs_workspace_bytes(4, 4, 100, 128, 1) == 0
 
 

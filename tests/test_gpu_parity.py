@@ -47,10 +47,12 @@ def _run_prologue(X_bits, perm, i8=False, group=128):
     rrs.rrs_rotate_smooth_quant(X, p, Xq, Xop, xs, sg, chan_max=cm, group=group, i8=i8)
     # the operand-only call (Xq = NULL) is the rrs_linear hot path, which takes a separate code path in the
     # quantisation kernel: its bytes must be identical
-    Xop2 = torch.empty_like(Xop)
-    rrs.rrs_rotate_smooth_quant(X, p, None, Xop2, torch.empty_like(xs), torch.empty_like(sg), group=group, i8=i8)
+    # (and, for prefill K = 2^m, the group-max fused prologue: no chan_max requested)
+    Xop2, xs2, sg2 = torch.empty_like(Xop), torch.empty_like(xs), torch.empty_like(sg)
+    rrs.rrs_rotate_smooth_quant(X, p, None, Xop2, xs2, sg2, group=group, i8=i8)
     torch.cuda.synchronize()
     assert torch.equal(Xop, Xop2)
+    assert torch.equal(xs, xs2) and torch.equal(sg, sg2)
     return dict(Xq=Xq.cpu().numpy(), Xop=Xop.cpu().numpy(), Xq8=decode_operand(Xop.cpu().numpy(), i8),
                 alpha=xs.cpu().numpy(), s_group=sg.cpu().numpy(), chan_max=cm.cpu().numpy())
 

@@ -177,3 +177,64 @@ def test_full_size_c3_up_full_rows():
     Yref = o.scale_accumulate(P, s, a, beta, 1.0 / w.K)
     ref = dict(P=P, s_group=s, alpha=a, beta=beta, out_scale=1.0 / w.K, Y=Yref)
     assert bf16_ulp_error(Y.float().cpu().numpy()[rows], Yref, ref) <= 1.0
+
+
+# --------------------------------------------------------------------------- group-max fused prologue (round 2)
+
+@pytest.mark.parametrize("K,T,profile,group", [(4096, 2500, "channel", 128), (1024, 3001, "spike", 32),
+                                               (8192, 700, "mixed", 256), (128, 4099, "tiny", 32),
+                                               (16384, 300, "channel", 128), (2048, 65, "spike", 64)])
+def test_fused_group_prologue_bitexact(K, T, profile, group):
+    """The prefill prologue without a chan_max output (the rrs_linear hot path) reduces group maxima only
+    (s_g = max over tokens and the group's channels, Eq. 1-2): s_g, alpha and every code equal the
+    oracle's, at sizes with many row tiles per CTA and ragged last tiles."""
+    X_bits = make_activations(profile, T, K, 1900 + K % 89, 1901)
+    perm = _perm(make_activations(profile, 64, K, 1900 + K % 89, 1902))
+    Xr = o.rotate(bf16_bits_to_f64(X_bits))
+    s = o.group_scales(o.channel_max(Xr), perm, group)
+    q, a = o.smooth_quant(Xr, perm, s, group)
+    X, p = dev_bf16(X_bits), _dev(perm)
+    Xop = torch.empty((T, K), dtype=torch.uint8, device=DEV)
+    Xq = torch.empty((T, K // 2), dtype=torch.uint8, device=DEV)
+    xs = torch.empty(T, dtype=torch.float32, device=DEV)
+    sg = torch.empty(K // group, dtype=torch.float32, device=DEV)
+    for i8 in (False, True):
+        rrs.rrs_rotate_smooth_quant(X, p, Xq, Xop, xs, sg, group=group, i8=i8)
+        torch.cuda.synchronize()
+        assert np.array_equal(sg.cpu().numpy().view(np.uint32), s.view(np.uint32))
+        assert np.array_equal(xs.cpu().numpy().view(np.uint32), a.view(np.uint32))
+        assert np.array_equal(decode_operand(Xop.cpu().numpy(), i8), q)
+        assert np.array_equal(Xq.cpu().numpy(), o.pack_int4(q))
+
+
+def test_fused_group_prologue_slot_reuse_and_streams():
+    """The fused prologue keeps its group maxima and grid-barrier counters in library memory, one slot per call,
+    reset by the last CTA out: 600 calls (every slot reused twice) alternating two inputs on two streams must
+    reproduce the first results bit for bit."""
+    K, T = 1024, 900
+    ins = []
+    for k, prof in enumerate(("channel", "spike")):
+        X_bits = make_activations(prof, T, K, 1950 + k, 1951)
+        perm = _perm(make_activations(prof, 64, K, 1950 + k, 1952))
+        ins.append((dev_bf16(X_bits), _dev(perm)))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[torch.empty((T, K), dtype=torch.uint8, device=DEV), torch.empty(T, device=DEV),
+             torch.empty(K // 128, device=DEV),
+             torch.empty(rrs.rrs_workspace_bytes(T, 1, K, 128, 1), dtype=torch.uint8, device=DEV)] for _ in range(2)]
+    ref = []
+    for k in range(2):
+        rrs.rrs_rotate_smooth_quant(ins[k][0], ins[k][1], None, outs[k][0], outs[k][1], outs[k][2], ws=outs[k][3])
+        torch.cuda.synchronize()
+        ref.append([t.clone() for t in outs[k][:3]])
+    torch.cuda.synchronize()
+    for it in range(300):
+        for k in range(2):
+            with torch.cuda.stream(streams[k]):
+                for t in outs[k][:3]:
+                    t.zero_()
+                rrs.rrs_rotate_smooth_quant(ins[k][0], ins[k][1], None, outs[k][0], outs[k][1], outs[k][2],
+                                            ws=outs[k][3], stream=streams[k])
+    torch.cuda.synchronize()
+    for k in range(2):
+        for got, want in zip(outs[k][:3], ref[k]):
+            assert torch.equal(got, want)
