@@ -126,6 +126,22 @@ __global__ void dadd(int iters, unsigned long long* cycles, double* sink) {
   if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
 }
 
+// f32 -> f64 and f64 -> f32 (RN) conversions (the FWHT's input widening and output rounding): 8 chains, each step
+// one F2F.F64.F32 and one F2F.F32.F64
+__global__ void cvt64(int iters, unsigned long long* cycles, float* sink) {
+  float a[8];
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 0.25f + k;
+  unsigned long long t0 = clock64();
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __double2float_rn((double)a[k] * 1.0000001);
+  }
+  unsigned long long t1 = clock64();
+  float s = 0; for (int k = 0; k < 8; ++k) s += a[k];
+  sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+  if (threadIdx.x == 0) cycles[blockIdx.x] = t1 - t0;
+}
+
 __global__ void i2f(int iters, unsigned long long* cycles, float* sink) {
   int p[8]; float acc[8];
   for (int k = 0; k < 8; ++k) { p[k] = threadIdx.x * 7 + k; acc[k] = 0; }
@@ -191,7 +207,7 @@ int main() {
     double mx = 0; for (int i = 0; i < blocks; ++i) mx = mx > h[i] ? mx : (double)h[i];
     printf("%-28s %10.1f per clk per SM (cycles %.0f)\n", name, ops_per_block / mx, mx);
   };
-  for (int warps : {4, 8}) {
+  for (int warps : {4, 8, 12, 16, 32}) {
     int iters = 4096;
     tmem_ld_bw<<<nsm, warps * 32>>>(iters, cyc, (uint32_t*)sink); CK(cudaDeviceSynchronize());
     char nm[64]; snprintf(nm, 64, "tmem ld bytes (%d warps)", warps);
@@ -207,6 +223,8 @@ int main() {
     snprintf(nm, 64, "promo f32x2 elems (%d)", t); report(nm, nsm, (double)iters * 16 * t);
     dadd<<<nsm, t>>>(iters, cyc, (double*)sink); CK(cudaDeviceSynchronize());
     snprintf(nm, 64, "DADD lanes (%d thr)", t); report(nm, nsm, (double)iters * 16 * t);
+    cvt64<<<nsm, t>>>(iters, cyc, (float*)sink); CK(cudaDeviceSynchronize());
+    snprintf(nm, 64, "f32->f64->f32 + DMUL (%d)", t); report(nm, nsm, (double)iters * 8 * t);
     i2f<<<nsm, t>>>(iters, cyc, (float*)sink); CK(cudaDeviceSynchronize());
     snprintf(nm, 64, "I2F lanes (%d thr)", t); report(nm, nsm, (double)iters * 8 * t);
   }

@@ -309,9 +309,10 @@ static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* p
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "variant prologue kernels");
   }
   if (T > 0 && rrs::prologue_decode_supports(T, K, group)) {  // decode-sized T: one launch, no memset
+    // (without a chan_max output: the group-max variant, one grid barrier and no per-channel maxima)
     cudaError_t e = rrs::launch_prologue_decode(static_cast<const uint16_t*>(X), T, K, perm,
-                                                reinterpret_cast<unsigned*>(chan_max), Xr, s_group, Xq, Xq8, x_scale,
-                                                e4m3, group, st);
+                                                want_chan_max ? reinterpret_cast<unsigned*>(chan_max) : nullptr, Xr,
+                                                s_group, Xq, Xq8, x_scale, e4m3, group, st);
     return e == cudaSuccess ? RRS_OK : cuda_fail(e, "prologue_decode_kernel");
   }
   // prefill, K = 2^m: one cooperative launch that reduces group maxima only (s_g needs no per-channel c_j); a caller

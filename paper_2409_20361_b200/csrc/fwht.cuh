@@ -29,27 +29,31 @@ __host__ __device__ constexpr int ilog2_c(int n) { return n <= 1 ? 0 : 1 + ilog2
 __host__ __device__ constexpr int max_c(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int min_c(int a, int b) { return a < b ? a : b; }
 
-template <int K_>
+// B = index bits per register pass (E = 2^B doubles per thread).  B = 5: 128 registers of values' headroom for 16 warps
+// per SM, two transposes at K = 4096; B = 6 (2^m, K >= 4096): 64 doubles per thread, 8 warps per SM, one transpose
+// fewer (K = 4096 = 6 + 6 bits: a single shared-memory transpose per row).
+template <int K_, int B_ = 5>
 struct FwhtPlan {
   static constexpr int K = K_;
   static constexpr bool kPow2 = (K & (K - 1)) == 0;
   static constexpr int A = kPow2 ? 1 : 28;          // H28 factor
   static constexpr int NP2 = K / A;                  // power-of-two part
   static constexpr int LOGN = ilog2_c(NP2);
-  static constexpr int B = 5;                        // bits per pass (E = 32 doubles per thread)
+  static constexpr int B = B_;                       // bits per pass
   static constexpr int E = 1 << B;                   // values per thread in the 2^m passes
   static constexpr int TP2 = K / E;                  // threads per row in the 2^m passes
   static constexpr int TH28 = kPow2 ? 0 : NP2;       // threads per row in the H28 pass (one 28-vector each)
   static constexpr int TPR = max_c(TP2, TH28);       // threads per row
-  static constexpr int R = kPow2 ? max_c(1, 128 / TP2) : 1;  // rows per CTA tile (>= 4 warps per CTA)
+  static constexpr int R = kPow2 ? max_c(1, (B == 5 ? 128 : 64) / TP2) : 1;  // rows per CTA tile
   static constexpr int THREADS = ((R * TPR + 31) / 32) * 32;
-  static constexpr int MIN_BLOCKS = max_c(1, 512 / THREADS);  // 16 warps/SM -> <= 128 regs
+  static constexpr int MIN_BLOCKS = max_c(1, (B == 5 ? 512 : 256) / THREADS);  // B5: 16 warps/SM (<= 128 regs), B6: 8
   static constexpr int HI = LOGN - (B - 3);          // pass 0: bits [0,3) and [HI, LOGN)
   static constexpr int SLOTS = kPow2 ? E : 28;       // values per thread after the last pass
   static constexpr int TILE = R * K;                 // elements per CTA tile
-  // padding coefficients (tools/smem_pad_search.py): 2^m: i + i/16 + 4(i>>7); 28*512: i + i/16;
-  // 28*256: i + i/16 + 4(i>>6) + 4(i>>8)
-  static constexpr int PAD_S1 = kPow2 ? 7 : 6, PAD_C1 = (kPow2 || NP2 <= 256) ? 4 : 0;
+  // padding coefficients (tools/smem_pad_search.py): B5 2^m: i + i/16 + 4(i>>7); B6 2^m (K >= 4096):
+  // i + i/16 + 4(i>>8); 28*512: i + i/16; 28*256: i + i/16 + 4(i>>6) + 4(i>>8)
+  static_assert(B == 5 || (kPow2 && K >= 4096), "B = 6 plans: K = 2^m >= 4096");
+  static constexpr int PAD_S1 = kPow2 ? (B == 5 ? 7 : 8) : 6, PAD_C1 = (kPow2 || NP2 <= 256) ? 4 : 0;
   static constexpr int PAD_S2 = kPow2 ? 9 : 8, PAD_C2 = (!kPow2 && NP2 <= 256) ? 4 : 0;
   static constexpr int TILE_PAD = TILE + TILE / 16 + PAD_C1 * (TILE >> PAD_S1) + PAD_C2 * (TILE >> PAD_S2) + 8;
   static_assert(A * NP2 == K, "K must be 2^m or 28*2^m");

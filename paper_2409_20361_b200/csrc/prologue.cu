@@ -31,6 +31,7 @@ RRS_DEVICE void trace(int k, int slot) {
     g_trace[k][blockIdx.x][slot] = t;
   }
 }
+void copy_prologue_trace(void* dst, size_t bytes) { cudaMemcpyFromSymbol(dst, g_trace, bytes); }
 #else
 RRS_DEVICE void trace(int, int) {}
 #endif
@@ -332,39 +333,53 @@ constexpr int kGroupSlots = 256;
 constexpr int kMaxG = 160;  // api.cu kMaxGroups
 __device__ unsigned g_group_gmax[kGroupSlots][kMaxG];
 __device__ unsigned g_group_bar[kGroupSlots][2];  // [arrive (clusters), depart (CTAs)]
+// gmax / barrier slot per call (every prologue that uses the library slots): concurrent calls use different slots
+static unsigned next_slot() {
+  static std::atomic<unsigned> calls{0};
+  return calls.fetch_add(1u, std::memory_order_relaxed) % kGroupSlots;
+}
+
+// FWHT plan of the fused kernel: 64 doubles per thread (one transpose per row at K = 4096) where the plan exists
+template <int K>
+struct GroupPlan {
+  using P = FwhtPlan<K, (K >= 4096 ? 6 : 5)>;
+};
 
 template <int K>
 struct GroupSmem {
-  using P = FwhtPlan<K>;
+  using P = typename GroupPlan<K>::P;
   static constexpr int TPQ = K / 32;                                      // gather chunks per row
+  static constexpr int CH = TPQ / P::TP2;                                 // gather chunks per thread
   static constexpr int TILE_D = ((P::TILE_PAD * 8 + 127) / 128) * 128;  // fp64 transposes, then the f32 X~ tile
   static constexpr int STAGE = P::TILE * 2;                             // the bf16 tile (single buffer)
-  static constexpr int TBL = P::TILE * 2;                               // 32 u16 offsets per thread
+  static constexpr int TBL = P::TILE * 2;                               // 32 u16 offsets per gather chunk
   static constexpr int BYTES = TILE_D + STAGE + TBL + kMaxG * 4 + 2 * 32 * 4 + 16;  // + gmax, red[2][32], barrier
-  static_assert(P::kPow2 && P::E == 32 && P::THREADS == P::R * TPQ, "one gather chunk per thread per tile row");
+  static_assert(P::kPow2 && P::THREADS == P::R * P::TP2 && CH * P::TP2 == TPQ && CH <= 2, "gather chunks");
   static_assert(P::TILE * 4 <= TILE_D && P::TILE * 4 <= 65536, "f32 X~ tile overlays the transposes; u16 offsets");
 };
 
 template <int K>
-__global__ void __cluster_dims__(colmax_cluster<K>(), 1, 1) __launch_bounds__(FwhtPlan<K>::THREADS, FwhtPlan<K>::MIN_BLOCKS)
+__global__ void __cluster_dims__(colmax_cluster<K>(), 1, 1)
+    __launch_bounds__(GroupPlan<K>::P::THREADS, GroupPlan<K>::P::MIN_BLOCKS)
 prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restrict__ Xr,
                       const int32_t* __restrict__ perm, float* __restrict__ s_group_out, uint8_t* __restrict__ Xq,
                       int8_t* __restrict__ Xq8, float* __restrict__ scale_out, int e4m3, int group, unsigned slot) {
-  using P = FwhtPlan<K>;
+  using P = typename GroupPlan<K>::P;
   using S = GroupSmem<K>;
-  constexpr int TPQ = S::TPQ;
+  constexpr int TPQ = S::TPQ, CH = S::CH, TP2 = P::TP2;
   extern __shared__ __align__(128) uint8_t smem[];
   double* sm = reinterpret_cast<double*>(smem);
   float* xs = reinterpret_cast<float*>(smem);  // the f32 X~ tile [R][K], natural order (after the FWHT)
   uint16_t* stage = reinterpret_cast<uint16_t*>(smem + S::TILE_D);
-  uint4* tbl = reinterpret_cast<uint4*>(smem + S::TILE_D + S::STAGE);  // [4][THREADS] uint4 = 8 u16 offsets each
+  uint4* tbl = reinterpret_cast<uint4*>(smem + S::TILE_D + S::STAGE);  // [CH][4][THREADS] uint4 = 8 u16 offsets each
   unsigned* gmax_sm = reinterpret_cast<unsigned*>(smem + S::TILE_D + S::STAGE + S::TBL);
   float* red = reinterpret_cast<float*>(gmax_sm + kMaxG);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * 32);
   unsigned* gmax = g_group_gmax[slot];
   unsigned* gbar = g_group_bar[slot];
   const int tid = threadIdx.x;
-  const int rr = tid / TPQ, c = tid % TPQ, j0 = c * 32;  // this thread's gather chunk: row rr of a tile, j0..j0+31
+  // this thread's gather chunks: row rr of a tile, chunks c = cp + ch TP2 (positions 32 c .. 32 c + 31), ch < CH
+  const int rr = tid / TP2, cp = tid % TP2;
   const int G = K / group;
   const int64_t ntiles = (T + P::R - 1) / P::R;
 
@@ -380,7 +395,9 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   }
   __syncthreads();
   if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
-  {  // gather table: byte offset in xs of (row rr, column perm[j0 + k]), two per word (an offline input)
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch) {  // gather table: byte offset in xs of (row rr, column perm[j0 + k]), two per word
+    const int j0 = (cp + ch * TP2) * 32;
     const int4* pp = reinterpret_cast<const int4*>(perm + j0);
     uint32_t w[16];
 #pragma unroll
@@ -390,48 +407,63 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
       w[2 * q + 1] = (uint32_t)((rr * K + p4.z) * 4) | ((uint32_t)((rr * K + p4.w) * 4) << 16);
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tbl[q * P::THREADS + tid] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
-    for (int g = tid; g < kMaxG; g += P::THREADS) gmax_sm[g] = 0u;
+    for (int q = 0; q < 4; ++q)
+      tbl[(ch * 4 + q) * P::THREADS + tid] = make_uint4(w[4 * q], w[4 * q + 1], w[4 * q + 2], w[4 * q + 3]);
   }
+  for (int g = tid; g < kMaxG; g += P::THREADS) gmax_sm[g] = 0u;
   // (the table and gmax_sm are first read after the FWHT's barriers)
 
   // ---- pass 1
-  float gm = 0.0f;
+  trace(0, 0);
+  float gm[CH];
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch) gm[ch] = 0.0f;
   int rf, tf;  // (tile row, row-thread) of this thread in the FWHT's last layout
   tile_coords<P>(tid, rf, tf);
   float* xs_row = xs + rf * K;
   int it = 0;
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     ptx::mbar_wait(bar, it & 1);
-    double v[P::E];
-    int rr_, tp_;
-    fwht_tile<P>(stage, sm, v, rr_, tp_, [&](int j, float f) { xs_row[out_col<P>(tf, j)] = f; },
-                 [&] { if (tid == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x); });
-    __syncthreads();  // the X~ tile is complete
-    float z[32];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint4 o = tbl[q * P::THREADS + tid];
-      const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-      for (int h = 0; h < 4; ++h) {
-        z[8 * q + 2 * h] = *reinterpret_cast<const float*>(smem + (ow[h] & 0xFFFFu));
-        z[8 * q + 2 * h + 1] = *reinterpret_cast<const float*>(smem + (ow[h] >> 16));
-      }
+    if (it == 0) trace(0, 1);
+    {
+      double v[P::E];
+      int rr_, tp_;
+      fwht_tile<P>(stage, sm, v, rr_, tp_, [&](int j, float f) { xs_row[out_col<P>(tf, j)] = f; },
+                   [&] { if (tid == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x); });
     }
+    __syncthreads();  // the X~ tile is complete
+    float z[CH][32];
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 o = tbl[(ch * 4 + q) * P::THREADS + tid];
+        const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          z[ch][8 * q + 2 * h] = *reinterpret_cast<const float*>(smem + (ow[h] & 0xFFFFu));
+          z[ch][8 * q + 2 * h + 1] = *reinterpret_cast<const float*>(smem + (ow[h] >> 16));
+        }
+      }
     __syncthreads();  // every gather is done: the tile is rewritten by the next FWHT
     const int64_t trow = tile * P::R + rr;
     if (trow < T) {
-      float4* dst = reinterpret_cast<float4*>(Xr + trow * K) + c;
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        gm = fmaxf(gm, fmaxf(fmaxf(fabsf(z[4 * q]), fabsf(z[4 * q + 1])), fmaxf(fabsf(z[4 * q + 2]), fabsf(z[4 * q + 3]))));
-        dst[q * TPQ] = make_float4(z[4 * q], z[4 * q + 1], z[4 * q + 2], z[4 * q + 3]);
+      for (int ch = 0; ch < CH; ++ch) {
+        float4* dst = reinterpret_cast<float4*>(Xr + trow * K) + cp + ch * TP2;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          gm[ch] = fmaxf(gm[ch], fmaxf(fmaxf(fabsf(z[ch][4 * q]), fabsf(z[ch][4 * q + 1])),
+                                       fmaxf(fabsf(z[ch][4 * q + 2]), fabsf(z[ch][4 * q + 3]))));
+          dst[q * TPQ] = make_float4(z[ch][4 * q], z[ch][4 * q + 1], z[ch][4 * q + 2], z[ch][4 * q + 3]);
+        }
       }
     }
   }
   // ---- group maxima (values >= +0: unsigned order of the float bits is the float order)
-  atomicMax(gmax_sm + j0 / group, __float_as_uint(gm));
+  trace(0, 2);
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch) atomicMax(gmax_sm + (cp + ch * TP2) * 32 / group, __float_as_uint(gm[ch]));
   __syncthreads();
   for (int g = tid; g < G; g += P::THREADS)
     if (gmax_sm[g]) atomicMax(gmax + g, gmax_sm[g]);
@@ -450,6 +482,7 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
     }
   }
   ptx::cluster_sync();
+  trace(0, 3);
 
   // ---- pass 2
   for (int g = tid; g < G; g += P::THREADS) {
@@ -459,7 +492,10 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
     if (blockIdx.x == 0) s_group_out[g] = s;
   }
   __syncthreads();
-  const float inv_s = __frcp_rn(reinterpret_cast<const float*>(gmax_sm)[j0 / group]);  // R9
+  float inv_s[CH];
+#pragma unroll
+  for (int ch = 0; ch < CH; ++ch)  // R9
+    inv_s[ch] = __frcp_rn(reinterpret_cast<const float*>(gmax_sm)[(cp + ch * TP2) * 32 / group]);
   if (tid == 0) {  // this CTA has read gmax: the last CTA out resets the slot for a later call
     __threadfence();
     if (atomicAdd(&gbar[1], 1u) == gridDim.x - 1) {
@@ -472,33 +508,40 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, pr ^= 1) {
     const int64_t trow = tile * P::R + rr;
     const bool live = trow < T;
-    float z[32];
+    float z[CH][32];
     float m = 0.0f;
-    const float4* src = reinterpret_cast<const float4*>(Xr + (live ? trow : 0) * K) + c;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 x = live ? __ldcg(src + q * TPQ) : make_float4(0.f, 0.f, 0.f, 0.f);
-      z[4 * q] = __fmul_rn(x.x, inv_s);
-      z[4 * q + 1] = __fmul_rn(x.y, inv_s);
-      z[4 * q + 2] = __fmul_rn(x.z, inv_s);
-      z[4 * q + 3] = __fmul_rn(x.w, inv_s);
-      m = fmaxf(m, fmaxf(fmaxf(fabsf(z[4 * q]), fabsf(z[4 * q + 1])), fmaxf(fabsf(z[4 * q + 2]), fabsf(z[4 * q + 3]))));
+    for (int ch = 0; ch < CH; ++ch) {
+      const float4* src = reinterpret_cast<const float4*>(Xr + (live ? trow : 0) * K) + cp + ch * TP2;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 x = live ? __ldcg(src + q * TPQ) : make_float4(0.f, 0.f, 0.f, 0.f);
+        z[ch][4 * q] = __fmul_rn(x.x, inv_s[ch]);
+        z[ch][4 * q + 1] = __fmul_rn(x.y, inv_s[ch]);
+        z[ch][4 * q + 2] = __fmul_rn(x.z, inv_s[ch]);
+        z[ch][4 * q + 3] = __fmul_rn(x.w, inv_s[ch]);
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(z[ch][4 * q]), fabsf(z[ch][4 * q + 1])),
+                           fmaxf(fabsf(z[ch][4 * q + 2]), fabsf(z[ch][4 * q + 3]))));
+      }
     }
-    if constexpr (TPQ <= 32) {
-      m = seg_max(m, TPQ);
-    } else {  // the row's TPQ / 32 warps through red[pr] (double-buffered: one barrier per tile)
+    if constexpr (TP2 <= 32) {
+      m = seg_max(m, TP2);
+    } else {  // the row's TP2 / 32 warps through red[pr] (double-buffered: one barrier per tile)
       m = seg_max(m, 32);
       float* rb = red + pr * 32;
       if ((tid & 31) == 0) rb[tid >> 5] = m;
       __syncthreads();
-      const int w0 = (rr * TPQ) >> 5;
+      const int w0 = (rr * TP2) >> 5;
       float mm = 0.0f;
 #pragma unroll 4
-      for (int w = 0; w < TPQ / 32; ++w) mm = fmaxf(mm, rb[w0 + w]);
+      for (int w = 0; w < TP2 / 32; ++w) mm = fmaxf(mm, rb[w0 + w]);
       m = mm;
     }
-    if (live) write_codes(z, m, trow, K, j0, Xq, Xq8, scale_out, e4m3 != 0, false);
+    if (live)
+#pragma unroll
+      for (int ch = 0; ch < CH; ++ch) write_codes(z[ch], m, trow, K, (cp + ch * TP2) * 32, Xq, Xq8, scale_out, e4m3 != 0, false);
   }
+  trace(0, 4);
   ptx::pdl_launch_dependents();
 }
 
@@ -600,6 +643,21 @@ RRS_DEVICE void grid_barrier_selfclean(unsigned* bar, unsigned nblocks) {
       bar[0] = 0u;
       bar[1] = 0u;
     }
+  }
+  __syncthreads();
+}
+
+// As above, but the departure count (bar[1]) is left to the caller, which resets the slot after its last read of the
+// data the barrier published.
+RRS_DEVICE void grid_barrier_selfclean_keep(unsigned* bar, unsigned nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(&bar[0], 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < nblocks);
   }
   __syncthreads();
 }
@@ -740,10 +798,103 @@ prologue_decode_kernel(const uint16_t* __restrict__ X, int T, const int32_t* __r
   trace(2, 6);
 }
 
+// The decode prologue without a chan_max output (the rrs_linear hot path).  s_g = max over (t, j' in g) of |X~_{t,perm[j']}|
+// (Eq. 1-2 P:90-91 with the reorder P:106) is a joint max over tokens and the group's channels, so the CTAs never form
+// c_j: each CTA gathers its row in reordered order, reduces its group maxima over the group's L/32 lanes and folds them
+// into gmax[G] (library memory, one red.max per group per CTA); one grid barrier; every thread reads its group's s_g.
+// T = 1 needs no barrier at all (the row's group maxima are s_g).  gmax and the barrier counters are per-call slots,
+// zero at module load and reset by the last CTA to leave (no memset launch).
+template <int C>
+__global__ void __launch_bounds__(C * 32)
+prologue_decode_group_kernel(const uint16_t* __restrict__ X, const int32_t* __restrict__ perm,
+                             float* __restrict__ s_group_out, uint8_t* __restrict__ Xq, int8_t* __restrict__ Xq8,
+                             float* __restrict__ scale_out, int e4m3, int group, unsigned slot) {
+  constexpr int K = C * 1024, TPR = K / 32;
+  using S = DecodePrologueSmem<C>;
+  extern __shared__ __align__(128) uint8_t smem[];
+  double* tr = reinterpret_cast<double*>(smem);
+  double* y1 = reinterpret_cast<double*>(smem + S::TR);
+  float* xs = reinterpret_cast<float*>(smem);  // X~ row (natural column order), after phase A
+  uint16_t* xrow = reinterpret_cast<uint16_t*>(smem + S::TR + S::Y1);
+  float* red = reinterpret_cast<float*>(smem + S::TR + S::Y1 + S::XB);
+  uint64_t* bar_x = reinterpret_cast<uint64_t*>(smem + S::TR + S::Y1 + S::XB + 64 * 4);
+  ptx::pdl_launch_dependents();  // the decode GEMM may get resident (and start its W stream) on the SMs left free
+  const int tid = threadIdx.x;
+  const int t = blockIdx.x;
+  const int j0 = tid * 32;
+  if (tid == 0) {  // the whole bf16 row in one bulk copy
+    ptx::mbar_init(bar_x, 1);
+    ptx::fence_barrier_init();
+    ptx::mbar_arrive_expect_tx(bar_x, S::XB);
+    ptx::bulk_load(xrow, X + (int64_t)t * K, S::XB, bar_x);
+  }
+  trace(2, 0);
+  int pj[32];
+  load_perm32(perm, j0, pj);  // an offline input
+  __syncthreads();
+  ptx::mbar_wait(bar_x, 0);
+  trace(2, 1);
+  // ---- a1 (X~ rounded once to f32, natural column order, into xs over the idle transposes)
+  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i] = __double2float_rn(d); });
+  __syncthreads();
+  trace(2, 2);
+  // ---- a2 + a4: this row's maximum over each group of reordered positions (32 | group: a thread's chunk is in one group)
+  float m = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 32; ++k) m = fmaxf(m, fabsf(xs[pj[k]]));
+  m = seg_max(m, group >> 5);
+  const int g = j0 / group;
+  if (gridDim.x > 1) {
+    unsigned* gmax = g_group_gmax[slot];
+    unsigned* gbar = g_group_bar[slot];
+    if (j0 % group == 0) atomicMax(gmax + g, __float_as_uint(m));  // float bits of values >= +0
+    grid_barrier_selfclean_keep(gbar, gridDim.x);
+    trace(2, 3);
+    m = __uint_as_float(__ldcg(gmax + g));
+    __syncthreads();  // every thread of this CTA has read gmax
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(&gbar[1], 1u) == gridDim.x - 1) {  // the last CTA to leave resets the slot for a later call
+        for (int i = 0; i < K / group; ++i) gmax[i] = 0u;
+        gbar[0] = 0u;
+        gbar[1] = 0u;
+      }
+    }
+  }
+  if (m == 0.0f) m = 1.0f;  // R8
+  if (blockIdx.x == 0 && j0 % group == 0) s_group_out[g] = m;
+  trace(2, 4);
+  // ---- a3, a5, a6 on this CTA's row
+  quant_row<TPR>(xs, pj, __frcp_rn(m), true, red, tid, 0, t, gridDim.x, K, j0, Xq, Xq8, scale_out, e4m3 != 0, [] {});
+  trace(2, 6);
+}
+
+template <int C>
+static cudaError_t launch_decode_group_k(const uint16_t* X, int64_t T, const int32_t* perm, float* s_group, uint8_t* Xq,
+                                         int8_t* Xq8, float* scale, bool e4m3, int group, unsigned slot, cudaStream_t st) {
+  auto kern = prologue_decode_group_kernel<C>;
+  constexpr int smem = DecodePrologueSmem<C>::BYTES;
+  cudaError_t e = prepare_kernel(kern, smem, C * 32);
+  if (e != cudaSuccess) return e;
+  int ei = (int)e4m3;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)T);
+  cfg.blockDim = dim3(C * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // the grid barrier needs every CTA resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = T > 1 ? 1 : 0;  // a single row needs no barrier
+  return cudaLaunchKernelEx(&cfg, kern, X, perm, s_group, Xq, Xq8, scale, ei, group, slot);
+}
+
 template <int C>
 static cudaError_t launch_decode_prologue_k(const uint16_t* X, int64_t T, const int32_t* perm, unsigned* cm,
                                             float* scratch, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale,
                                             bool e4m3, int group, unsigned slot, cudaStream_t st) {
+  if (cm == nullptr) return launch_decode_group_k<C>(X, T, perm, s_group, Xq, Xq8, scale, e4m3, group, slot, st);
   auto kern = prologue_decode_kernel<C>;
   constexpr int smem = DecodePrologueSmem<C>::BYTES;
   cudaError_t e = prepare_kernel(kern, smem, C * 32);
@@ -778,8 +929,7 @@ bool prologue_decode_supports(int64_t T, int64_t K, int group) {
 cudaError_t launch_prologue_decode(const uint16_t* X, int64_t T, int64_t K, const int32_t* perm, unsigned* chan_max_bits,
                                    float* scratch, float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3,
                                    int group, cudaStream_t st) {
-  static std::atomic<unsigned> calls{0};  // barrier slot per call: concurrent calls use different counters
-  const unsigned slot = calls.fetch_add(1u, std::memory_order_relaxed);
+  const unsigned slot = next_slot();
   switch (K) {
 #define RRS_CASE(c) case c * 1024: return launch_decode_prologue_k<c>(X, T, perm, chan_max_bits, scratch, s_group, Xq, Xq8, scale, e4m3, group, slot, st);
     RRS_CASE(1) RRS_CASE(2) RRS_CASE(4) RRS_CASE(8)
@@ -952,7 +1102,7 @@ template <int K>
 static cudaError_t launch_group_k(const uint16_t* X, int64_t T, float* Xr, const int32_t* perm, float* s_group,
                                   uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int group, unsigned slot,
                                   cudaStream_t st) {
-  using P = FwhtPlan<K>;
+  using P = typename GroupPlan<K>::P;
   auto kern = prologue_group_kernel<K>;
   const int smem = GroupSmem<K>::BYTES;
   cudaError_t e = prepare_kernel(kern, smem, P::THREADS);
@@ -1006,8 +1156,7 @@ cudaError_t launch_prologue_fused(const uint16_t* X, int64_t T, int64_t K, float
                                   float* s_group, uint8_t* Xq, int8_t* Xq8, float* scale, bool e4m3, int group,
                                   cudaStream_t st) {
   if (K / group > kMaxG) return cudaErrorInvalidValue;
-  static std::atomic<unsigned> calls{0};  // gmax / barrier slot per call: concurrent calls use different slots
-  const unsigned slot = calls.fetch_add(1u, std::memory_order_relaxed) % kGroupSlots;
+  const unsigned slot = next_slot();
   switch (K) {
 #define RRS_CASE(k) case k: return launch_group_k<k>(X, T, Xr, perm, s_group, Xq, Xq8, scale, e4m3, group, slot, st);
     RRS_FOR_EACH_POW2_K(RRS_CASE)

@@ -95,7 +95,10 @@ def test_hot_kernels_do_not_spill(lib_path):
     out = subprocess.run(["cuobjdump", "-res-usage", lib_path], capture_output=True, text=True).stdout
     hot = ["rrs_gemm_kernelILb0ELb0ELb0ELi2ELb1ELb0E",   # RRS GEMM, bf16 Y, CTA pairs, E4M3 (the headline)
            "rrs_gemm_kernelILb1ELb0ELb0ELi2ELb1ELb0E",   # plain per-channel baseline
-           "fwht_colmax_kernelILi14336E", "smooth_quant_kernelILi14336E", "smooth_quant_kernelILi4096E"]
+           "fwht_colmax_kernelILi14336E", "smooth_quant_kernelILi14336E", "smooth_quant_kernelILi4096E",
+           "prologue_group_kernelILi4096E",                # fused prefill prologue (the headline's)
+           "rrs_decode_gemm_kernelILi64E", "rrs_decode_gemm_kernelILi16E",  # decode GEMM (configs[3])
+           "prologue_decode_group_kernelILi8E"]            # decode prologue (configs[3])
     usage = {}
     lines = out.splitlines()
     for i, l in enumerate(lines):
