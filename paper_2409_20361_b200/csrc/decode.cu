@@ -48,6 +48,7 @@ __device__ __forceinline__ void dtrace(int ev, int i) {
 }
 // experiment knobs of the timeline harness: bit 0 = load X only for the first ring round (W-stream-only timing)
 __device__ int g_dec_exp = 0;
+int g_dec_no_pdl = 0;  // host: launch the GEMM without programmatic dependent launch
 #else
 __device__ __forceinline__ void dtrace(int, int) {}
 #endif
@@ -59,12 +60,14 @@ constexpr int KBLK = 128;                // codes per K-block
 constexpr int TILE4 = 256 * KBLK / 2;    // one decode4 tile in HBM (256 rows x one K-block, 16 KiB)
 constexpr int W_STAGE = ROWS * KBLK / 2; // this CTA's half of a tile: 8 KiB, contiguous (rows at 64 bytes)
 constexpr int NS = 16;                   // W ring stages (128 KiB in flight)
-constexpr int NA = 4;                    // TMEM A stages (widened W)
-constexpr int NCONV = 8, NPROM = 4;      // two converter sets (even / odd K-blocks) x 4 lane quadrants
+constexpr int NA = 8;                    // TMEM A stages (widened W): 8 K-blocks between conversion and MMA
+constexpr int NACC = 4;                  // TMEM accumulator buffers (groups in flight between MMA and promotion)
+constexpr int NCONV = 8, NPROM = 8;      // two converter sets (even / odd K-blocks) x 4 lane quadrants; promotion:
+                                         // 4 lane quadrants x 2 column halves
 constexpr int W_PROD = 0, MMA_WARP = 1, CONV0 = 2, PROM0 = CONV0 + NCONV, X_PROD = PROM0 + NPROM;
 constexpr int THREADS = (X_PROD + 1) * 32;
-constexpr int A_COL0 = 128;              // TMEM columns [128, 128 + 32 NA): A stages; [0, 2 TP): accumulators
-constexpr int TMEM_COLS = 256;
+constexpr int A_COL0 = 256;              // TMEM columns [256, 256 + 32 NA): A stages; [0, NACC TP): accumulators
+constexpr int TMEM_COLS = 512;
 constexpr int MAX_G = 160;
 
 template <int TP>
@@ -117,8 +120,8 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   uint64_t* afull = xempty + NX;
   uint64_t* aempty = afull + NA;
   uint64_t* tfull = aempty + NA;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* redbar = tempty + 2;     // the peers' partial slices have landed (bulk copies, complete_tx)
+  uint64_t* tempty = tfull + NACC;
+  uint64_t* redbar = tempty + NACC;     // the peers' partial slices have landed (bulk copies, complete_tx)
   uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(redbar + 1);
   float* s_sm = reinterpret_cast<float*>(smem + C::RING + 1024);
   float* xs_sm = s_sm + MAX_G;   // alpha_t * out_scale, t < T
@@ -137,6 +140,11 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   const int ng = nkb / p.gpb;
   const int g0 = kb0 / p.gpb;
   const int rows_per = ROWS / S;
+  // every row block walks its K range starting at a different group (rotated by the row block): the X tiles are shared
+  // by all row blocks, and 64 CTAs requesting the same 8 KiB at the same moment serialise on its L2 lines (measured:
+  // 2.4 us per X load).  The group order of the promotion differs per row block but is fixed (R15).
+  const int rot = rb % ng;
+  auto kb_at = [&](int i) { return ((i / p.gpb + rot) % ng) * p.gpb + i % p.gpb; };  // loop index -> K-block (CTA range)
 
   static_assert(NX <= 16 && NS <= 16, "barrier area");
   if (warp == 0 && lane == 0) {
@@ -153,7 +161,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       ptx::mbar_init(&afull[a], 4);
       ptx::mbar_init(&aempty[a], 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NACC; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], NPROM);
     }
@@ -176,7 +184,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
         const int s = i % NS;
         ptx::mbar_wait(&wempty[s], ((i / NS) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&wfull[s], W_STAGE);
-        ptx::bulk_load(wring + s * W_STAGE, wsrc + (int64_t)i * TILE4, W_STAGE, &wfull[s]);
+        ptx::bulk_load(wring + s * W_STAGE, wsrc + (int64_t)kb_at(i) * TILE4, W_STAGE, &wfull[s]);
         dtrace(0, i);
       }
     }
@@ -194,7 +202,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
         }
 #endif
         ptx::mbar_arrive_expect_tx(&xfull[s], C::X_STAGE);
-        ptx::tma_load_2d(xring + s * C::X_STAGE, &tmap_x, &xfull[s], (kb0 + i) * KBLK, 0, ptx::kEvictLast);
+        ptx::tma_load_2d(xring + s * C::X_STAGE, &tmap_x, &xfull[s], (kb0 + kb_at(i)) * KBLK, 0, ptx::kEvictLast);
         dtrace(1, i);
       }
     }
@@ -206,8 +214,8 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       for (int i = 0; i < nkb; ++i) {
         const int s = i % NX, a = i % NA;
         const int gl = i / p.gpb, kin = i % p.gpb;
-        const uint32_t b = gl & 1;
-        if (kin == 0) ptx::mbar_wait(&tempty[b], ((gl >> 1) & 1) ^ 1);
+        const uint32_t b = gl % NACC;
+        if (kin == 0) ptx::mbar_wait(&tempty[b], ((gl / NACC) & 1) ^ 1);
         ptx::mbar_wait(&afull[a], (i / NA) & 1);
         ptx::mbar_wait(&xfull[s], (i / NX) & 1);
         ptx::tc_fence_after();
@@ -230,11 +238,12 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     const int q = warp & 3, set = (int)(warp - CONV0) >> 2;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     const int r = q * 32 + lane;
+    // software-pipelined: the tcgen05.st of tile i completes (wait::st, then afull) only after tile i + 2 has been read
+    // and widened, so the store's latency overlaps the next tile's shared-memory loads and ALU work
+    int prev_a = -1;
     for (int i = set; i < nkb; i += 2) {
       const int s = i % NS, a = i % NA;
       ptx::mbar_wait(&wfull[s], (i / NS) & 1);
-      ptx::mbar_wait(&aempty[a], ((i / NA) & 1) ^ 1);
-      ptx::tc_fence_after();
       // the tile is stored pre-swizzled: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3), so every
       // quarter-warp's 16-byte loads hit 8 distinct bank groups (r and the tile row differ by a multiple of 128)
       const uint8_t* rowp = wring + s * W_STAGE + r * 64;
@@ -251,48 +260,65 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       }
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&wempty[s]);  // the W stage is in registers: the producer may refill it
+      if (prev_a >= 0) {  // the previous tile's store has had this tile's loads to complete
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          ptx::mbar_arrive(&afull[prev_a]);
+          if (warp == CONV0) dtrace(2, i - 2);
+        }
+      }
+      ptx::mbar_wait(&aempty[a], ((i / NA) & 1) ^ 1);
+      ptx::tc_fence_after();
       RRS_TMEM_ST32(tmem + lane_off + A_COL0 + a * 32, v);
+      prev_a = a;
+    }
+    if (prev_a >= 0) {
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) {
-        ptx::mbar_arrive(&afull[a]);
-        if (warp == CONV0) dtrace(2, i);
-      }
+      if (lane == 0) ptx::mbar_arrive(&afull[prev_a]);
     }
   } else if (warp < X_PROD) {
     // ------------------------------------------------------------------ promotion
-    const int q = warp & 3;
+    // warp = lane quadrant q (warp % 4) x column half ch: TP / 2 token columns of 32 W rows; all its TMEM loads of a
+    // group are issued before one wait (the loads' latency, not their bandwidth, paced the MMA with two buffers)
+    constexpr int TH = TP / 2 < 16 ? 16 : TP / 2;  // columns per warp (TP = 16: the second half has none)
+    const int q = warp & 3, ch = (int)(warp - PROM0) >> 2;
+    const bool cols = ch * TH < TP;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     ptx::pdl_wait();  // s_g come from the prologue
     for (int g = threadIdx.x - PROM0 * 32; g < ng; g += NPROM * 32) s_sm[g] = p.s_group[g0 + g];
     {  // the epilogue's scales, read once here (off the critical path)
-      const int i = threadIdx.x - PROM0 * 32;  // 0 .. 127
+      const int i = threadIdx.x - PROM0 * 32;  // 0 .. 255
       if (i < p.T) xs_sm[i] = p.x_scale[i] * p.out_scale;
-      ws_sm[i] = row0 + i < p.N ? p.w_scale[row0 + i] : 0.0f;
+      if (i < ROWS) ws_sm[i] = row0 + i < p.N ? p.w_scale[row0 + i] : 0.0f;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(NPROM * 32));
-    float acc[TP];  // sum_g s_g P_g of this thread's W row for the TP token columns
+    float acc[TH];  // sum_g s_g P_g of this thread's W row for this warp's token columns
 #pragma unroll
-    for (int t = 0; t < TP; ++t) acc[t] = 0.0f;
+    for (int t = 0; t < TH; ++t) acc[t] = 0.0f;
     for (int gl = 0; gl < ng; ++gl) {
-      const uint32_t b = gl & 1;
-      ptx::mbar_wait(&tfull[b], (gl >> 1) & 1);
+      const uint32_t b = gl % NACC;
+      ptx::mbar_wait(&tfull[b], (gl / NACC) & 1);
       ptx::tc_fence_after();
       if (warp == PROM0 && lane == 0) dtrace(4, gl);
-      const float sc = s_sm[gl] * 0.0625f;  // s_g / 16 (exact: the widened codes are 16 q)
+      const float sc = s_sm[(gl + rot) % ng] * 0.0625f;  // s_g / 16 (exact: the widened codes are 16 q)
+      uint32_t v[TH];
+      if (cols) {
 #pragma unroll
-      for (int c = 0; c < TP / 16; ++c) {
-        uint32_t v[16];
-        RRS_TMEM_LD16(tmem + lane_off + b * TP + c * 16, v);
+        for (int c = 0; c < TH / 16; ++c) RRS_TMEM_LD16(tmem + lane_off + b * TP + ch * TH + c * 16, (v + 16 * c));
         RRS_TMEM_WAIT_LD16(v);
-        if (c == TP / 16 - 1) {
-          ptx::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(&tempty[b]);
-        }
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[c * 16 + j] = fmaf(sc, (float)(int)v[j], acc[c * 16 + j]);
+        for (int c = 1; c < TH / 16; ++c) RRS_REG_FENCE16((v + 16 * c));
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+      if (cols) {
+#pragma unroll
+        for (int j = 0; j < TH; ++j) acc[j] = fmaf(sc, (float)(int)v[j], acc[j]);
       }
     }
     // every MMA has completed (this warp saw the last tfull), so every converter and every ring stage of this CTA
@@ -301,11 +327,13 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     if (warp == PROM0 && lane == 0) dtrace(7, 0);
     asm volatile("barrier.sync 2, %0;" ::"n"(THREADS) : "memory");
     const int r = q * 32 + lane;
+    if (cols) {
 #pragma unroll
-    for (int t4 = 0; t4 < TP / 4; ++t4)
-      if (4 * t4 < p.T)
-        *reinterpret_cast<float4*>(part + r * (TP + 4) + 4 * t4) =
-            make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
+      for (int t4 = 0; t4 < TH / 4; ++t4)
+        if (ch * TH + 4 * t4 < p.T)
+          *reinterpret_cast<float4*>(part + r * (TP + 4) + ch * TH + 4 * t4) =
+              make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
+    }
     ptx::fence_proxy_async_shared();
   }
   // the other warps' arrival at that CTA barrier (non-aligned form: producer lanes may still be diverged)
@@ -409,14 +437,17 @@ static cudaError_t launch_decode_tp(const CUtensorMap& tx, const DecodeParams& p
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  attr[1].id = cudaLaunchAttributeClusterDimension;
-  attr[1].val.clusterDim.x = p.S;
-  attr[1].val.clusterDim.y = 1;
-  attr[1].val.clusterDim.z = 1;
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.S;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
+#ifdef RRS_TRACE
+  if (g_dec_no_pdl) cfg.numAttrs = 1;  // timeline experiment: the GEMM starts only after the prologue has finished
+#endif
   return cudaLaunchKernelEx(&cfg, kern, tx, p);
 }
 

@@ -24,14 +24,18 @@ namespace rrs {
 // records %globaltimer at fixed points into g_trace[kernel][cta][slot].
 #ifdef RRS_TRACE
 __device__ unsigned long long g_trace[3][1024][16];
+__device__ unsigned long long g_trace_clk[3][1024][16];  // the SM's clock64 at the same points (effective SM clock)
 RRS_DEVICE void trace(int k, int slot) {
   if (threadIdx.x == 0 && blockIdx.x < 1024 && slot < 16) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    unsigned long long t, c;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) :: "memory");
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(c) :: "memory");
     g_trace[k][blockIdx.x][slot] = t;
+    g_trace_clk[k][blockIdx.x][slot] = c;
   }
 }
 void copy_prologue_trace(void* dst, size_t bytes) { cudaMemcpyFromSymbol(dst, g_trace, bytes); }
+void copy_prologue_trace_clk(void* dst, size_t bytes) { cudaMemcpyFromSymbol(dst, g_trace_clk, bytes); }
 #else
 RRS_DEVICE void trace(int, int) {}
 #endif
@@ -332,7 +336,7 @@ RRS_DEVICE void quant_row(const float* xs, const int (&pj)[32], float inv_s, boo
 constexpr int kGroupSlots = 256;
 constexpr int kMaxG = 160;  // api.cu kMaxGroups
 __device__ unsigned g_group_gmax[kGroupSlots][kMaxG];
-__device__ unsigned g_group_bar[kGroupSlots][2];  // [arrive (clusters), depart (CTAs)]
+__device__ unsigned g_group_bar[kGroupSlots][3];  // [arrive (clusters), depart (CTAs), next row tile (dynamic rows)]
 // gmax / barrier slot per call (every prologue that uses the library slots): concurrent calls use different slots
 static unsigned next_slot() {
   static std::atomic<unsigned> calls{0};
@@ -353,9 +357,14 @@ struct GroupSmem {
   static constexpr int TILE_D = ((P::TILE_PAD * 8 + 127) / 128) * 128;  // fp64 transposes, then the f32 X~ tile
   static constexpr int STAGE = P::TILE * 2;                             // the bf16 tile (single buffer)
   static constexpr int TBL = P::TILE * 2;                               // 32 u16 offsets per gather chunk
-  static constexpr int BYTES = TILE_D + STAGE + TBL + kMaxG * 4 + 2 * 32 * 4 + 16;  // + gmax, red[2][32], barrier
+  static constexpr int MAX_TILES = 64;                                  // row tiles a CTA may claim (dynamic rows)
+  static constexpr int BYTES = TILE_D + STAGE + TBL + kMaxG * 4 + 2 * 32 * 4 + 16 + MAX_TILES * 8;
+  // + gmax, red[2][32], barrier, the CTA's tile list
   static_assert(P::kPow2 && P::THREADS == P::R * P::TP2 && CH * P::TP2 == TPQ && CH <= 2, "gather chunks");
-  static_assert(P::TILE * 4 <= TILE_D && P::TILE * 4 <= 65536, "f32 X~ tile overlays the transposes; u16 offsets");
+  // the f32 X~ tile is stored with one pad word per 32 (row stride K + K/32): a reorder that maps a warp's lanes to
+  // columns 32 apart (e.g. the identity) would otherwise put all 32 gathers of an instruction in one bank
+  static constexpr int KP = K + K / 32;
+  static_assert(P::R * KP * 4 <= TILE_D && P::R * KP < 65536, "padded f32 X~ tile overlays the transposes; u16 words");
 };
 
 template <int K>
@@ -369,12 +378,13 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   constexpr int TPQ = S::TPQ, CH = S::CH, TP2 = P::TP2;
   extern __shared__ __align__(128) uint8_t smem[];
   double* sm = reinterpret_cast<double*>(smem);
-  float* xs = reinterpret_cast<float*>(smem);  // the f32 X~ tile [R][K], natural order (after the FWHT)
+  float* xs = reinterpret_cast<float*>(smem);  // the f32 X~ tile [R][KP], natural order, padded (after the FWHT)
   uint16_t* stage = reinterpret_cast<uint16_t*>(smem + S::TILE_D);
-  uint4* tbl = reinterpret_cast<uint4*>(smem + S::TILE_D + S::STAGE);  // [CH][4][THREADS] uint4 = 8 u16 offsets each
+  uint4* tbl = reinterpret_cast<uint4*>(smem + S::TILE_D + S::STAGE);  // [CH][4][THREADS] uint4 = 8 u16 word indices
   unsigned* gmax_sm = reinterpret_cast<unsigned*>(smem + S::TILE_D + S::STAGE + S::TBL);
   float* red = reinterpret_cast<float*>(gmax_sm + kMaxG);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * 32);
+  int64_t* tiles_sm = reinterpret_cast<int64_t*>(bar + 2);  // [MAX_TILES]: the row tiles this CTA transformed
   unsigned* gmax = g_group_gmax[slot];
   unsigned* gbar = g_group_bar[slot];
   const int tid = threadIdx.x;
@@ -396,15 +406,16 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   __syncthreads();
   if (tid == 0 && blockIdx.x < ntiles) issue(blockIdx.x);
 #pragma unroll
-  for (int ch = 0; ch < CH; ++ch) {  // gather table: byte offset in xs of (row rr, column perm[j0 + k]), two per word
+  for (int ch = 0; ch < CH; ++ch) {  // gather table: word index in xs of (row rr, column perm[j0 + k]), two per word
     const int j0 = (cp + ch * TP2) * 32;
     const int4* pp = reinterpret_cast<const int4*>(perm + j0);
     uint32_t w[16];
+    auto wi = [&](int c) { return (uint32_t)(rr * S::KP + c + (c >> 5)); };
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int4 p4 = __ldg(pp + q);
-      w[2 * q] = (uint32_t)((rr * K + p4.x) * 4) | ((uint32_t)((rr * K + p4.y) * 4) << 16);
-      w[2 * q + 1] = (uint32_t)((rr * K + p4.z) * 4) | ((uint32_t)((rr * K + p4.w) * 4) << 16);
+      w[2 * q] = wi(p4.x) | (wi(p4.y) << 16);
+      w[2 * q + 1] = wi(p4.z) | (wi(p4.w) << 16);
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -414,22 +425,43 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   // (the table and gmax_sm are first read after the FWHT's barriers)
 
   // ---- pass 1
+  // Row tiles: the first is blockIdx.x; later ones are claimed from a counter in library memory (dynamic: a CTA that
+  // finishes early takes the next tile, so no CTA runs a whole extra tile behind the rest -- with the static stride
+  // 4096 rows over 568 CTAs gave 8 tiles to some and 7 to most), one claim ahead so the atomic's latency is hidden
+  // behind a whole tile.  The CTA records its tiles for pass 2.  Very long calls (more claims than the list holds) keep
+  // the static stride.
   trace(0, 0);
+  constexpr int MT = S::MAX_TILES;
+  const bool dyn = ntiles <= (int64_t)(MT / 2) * gridDim.x;
   float gm[CH];
 #pragma unroll
   for (int ch = 0; ch < CH; ++ch) gm[ch] = 0.0f;
   int rf, tf;  // (tile row, row-thread) of this thread in the FWHT's last layout
   tile_coords<P>(tid, rf, tf);
-  float* xs_row = xs + rf * K;
-  int it = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+  float* xs_row = xs + rf * S::KP;
+  int64_t cur = blockIdx.x, nxt = ntiles;  // (thread 0) this tile and the claimed next one
+  if (tid == 0 && cur < ntiles) nxt = dyn ? gridDim.x + (int64_t)atomicAdd(&gbar[2], 1u) : cur + gridDim.x;
+  int ntl = 0;
+  int64_t tile = blockIdx.x;
+  for (int it = 0; tile < ntiles; ++it) {
+    int64_t nn = ntiles;  // (thread 0) the tile after nxt, claimed now, used one tile later
+    if (tid == 0) {
+      tiles_sm[ntl] = cur;
+      tiles_sm[ntl + 1] = nxt;  // read by every thread after this tile's barriers
+      if (nxt < ntiles) nn = (dyn && ntl + 2 < MT - 1) ? gridDim.x + (int64_t)atomicAdd(&gbar[2], 1u)
+                                                        : (dyn ? (int64_t)ntiles : nxt + gridDim.x);
+    }
     ptx::mbar_wait(bar, it & 1);
     if (it == 0) trace(0, 1);
     {
       double v[P::E];
       int rr_, tp_;
-      fwht_tile<P>(stage, sm, v, rr_, tp_, [&](int j, float f) { xs_row[out_col<P>(tf, j)] = f; },
-                   [&] { if (tid == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x); });
+      fwht_tile<P>(stage, sm, v, rr_, tp_,
+                   [&](int j, float f) {
+                     const int c = out_col<P>(tf, j);
+                     xs_row[c + (c >> 5)] = f;
+                   },
+                   [&] { if (tid == 0 && nxt < ntiles) issue(nxt); });
     }
     __syncthreads();  // the X~ tile is complete
     float z[CH][32];
@@ -441,10 +473,11 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
         const uint32_t ow[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-          z[ch][8 * q + 2 * h] = *reinterpret_cast<const float*>(smem + (ow[h] & 0xFFFFu));
-          z[ch][8 * q + 2 * h + 1] = *reinterpret_cast<const float*>(smem + (ow[h] >> 16));
+          z[ch][8 * q + 2 * h] = xs[ow[h] & 0xFFFFu];
+          z[ch][8 * q + 2 * h + 1] = xs[ow[h] >> 16];
         }
       }
+    const int64_t next_tile = tiles_sm[ntl + 1];
     __syncthreads();  // every gather is done: the tile is rewritten by the next FWHT
     const int64_t trow = tile * P::R + rr;
     if (trow < T) {
@@ -459,6 +492,12 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
         }
       }
     }
+    ++ntl;
+    tile = next_tile;
+    if (tid == 0) {
+      cur = nxt;
+      nxt = nn;
+    }
   }
   // ---- group maxima (values >= +0: unsigned order of the float bits is the float order)
   trace(0, 2);
@@ -467,6 +506,22 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   __syncthreads();
   for (int g = tid; g < G; g += P::THREADS)
     if (gmax_sm[g]) atomicMax(gmax + g, gmax_sm[g]);
+
+  // pass 2 reads back exactly the values this thread stored in pass 1 (same rows, same chunks), so its first row is
+  // loaded before the grid barrier (program order makes the thread's own stores visible to its loads); later rows are
+  // prefetched one row ahead in registers
+  auto load_row = [&](int64_t tile, float4 (&x)[CH][8]) {
+    const int64_t trow = tile * P::R + rr;
+    const bool live = tile < ntiles && trow < T;
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch) {
+      const float4* src = reinterpret_cast<const float4*>(Xr + (live ? trow : 0) * K) + cp + ch * TP2;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[ch][q] = live ? __ldcg(src + q * TPQ) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  };
+  float4 xn[CH][8];
+  load_row(ntl > 0 ? tiles_sm[0] : ntiles, xn);
 
   // ---- grid barrier: the Xr stores and the gmax atomics are visible everywhere
   __threadfence();
@@ -502,20 +557,27 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
       for (int g = 0; g < G; ++g) gmax[g] = 0u;
       gbar[0] = 0u;
       gbar[1] = 0u;
+      gbar[2] = 0u;
     }
   }
   int pr = 0;
-  for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, pr ^= 1) {
+  for (int i = 0; i < ntl; ++i, pr ^= 1) {
+    const int64_t tile = tiles_sm[i];
     const int64_t trow = tile * P::R + rr;
     const bool live = trow < T;
+    float4 xc[CH][8];
+#pragma unroll
+    for (int ch = 0; ch < CH; ++ch)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) xc[ch][q] = xn[ch][q];
+    load_row(i + 1 < ntl ? tiles_sm[i + 1] : ntiles, xn);  // the next row's loads fly while this row is quantised
     float z[CH][32];
     float m = 0.0f;
 #pragma unroll
     for (int ch = 0; ch < CH; ++ch) {
-      const float4* src = reinterpret_cast<const float4*>(Xr + (live ? trow : 0) * K) + cp + ch * TP2;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 x = live ? __ldcg(src + q * TPQ) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 x = xc[ch][q];
         z[ch][4 * q] = __fmul_rn(x.x, inv_s[ch]);
         z[ch][4 * q + 1] = __fmul_rn(x.y, inv_s[ch]);
         z[ch][4 * q + 2] = __fmul_rn(x.z, inv_s[ch]);
@@ -831,11 +893,13 @@ prologue_decode_group_kernel(const uint16_t* __restrict__ X, const int32_t* __re
   trace(2, 0);
   int pj[32];
   load_perm32(perm, j0, pj);  // an offline input
+#pragma unroll
+  for (int k = 0; k < 32; ++k) pj[k] += pj[k] >> 5;  // xs keeps one pad word per 32 columns (no bank-aligned gathers)
   __syncthreads();
   ptx::mbar_wait(bar_x, 0);
   trace(2, 1);
-  // ---- a1 (X~ rounded once to f32, natural column order, into xs over the idle transposes)
-  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i] = __double2float_rn(d); });
+  // ---- a1 (X~ rounded once to f32, natural column order, padded, into xs over the idle transposes)
+  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i + (i >> 5)] = __double2float_rn(d); });
   __syncthreads();
   trace(2, 2);
   // ---- a2 + a4: this row's maximum over each group of reordered positions (32 | group: a thread's chunk is in one group)

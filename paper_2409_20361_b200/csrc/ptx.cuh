@@ -309,6 +309,16 @@ RRS_DEV void mma_commit(uint64_t* bar) {
                :                                                                                         \
                : "memory")
 
+// no-op that "redefines" 16 registers: placed after a tcgen05.wait::ld that covered several RRS_TMEM_LD16s, so the
+// compiler cannot move the uses of the other loads' registers above the wait either
+#define RRS_REG_FENCE16(r)                                                                               \
+  asm volatile(""                                                                                        \
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),     \
+                 "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), \
+                 "+r"(r[14]), "+r"(r[15])                                                                \
+               :                                                                                         \
+               : "memory")
+
 #define RRS_TMEM_ST16_SPLAT(taddr, v)                                                                    \
   asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" \
                ::"r"(taddr), "r"(v) : "memory")
