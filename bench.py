@@ -8,7 +8,7 @@
 A step is one pass of the whole hot path (a7 is the offline weight
 preparation, timed once and reported separately) over one batch of synthetic input already resident in HBM:
     rrs_rotate_smooth_quant -> rrs_gemm (-> rrs_allgather_columns when N > 1).
-L2 is flushed (256 MiB write) before every timed step; each step is timed with CUDA events on the launching
+L2 is flushed (256 MiB write + 256 MiB clean read, bench/l2flush.py) before every timed step; each step is timed with CUDA events on the launching
 stream and the bracketing barrier + synchronize surround the whole timed loop.  Multi-GPU times are the max
 over ranks.  Inputs: seeded synthetic LLaMA-like activations and N(0, 0.02^2) weights (rrs_synth).
 """
@@ -27,6 +27,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "bench"))
+from l2flush import L2Flush  # noqa: E402  (bench/l2flush.py)
 
 from rrs_synth import WORKLOADS, make_layer, make_weights  # noqa: E402
 
@@ -154,7 +156,7 @@ def measure_workload(args, wname, dev, world, rank, comm, cpu_base: bool, i8: bo
     pws = torch.empty(rrs.rrs_workspace_bytes(T, 1, K, 128, 1), dtype=torch.uint8, device=dev)
     Y_shard = torch.empty((T, n_local), dtype=out_dtype, device=dev)
     Y = torch.empty((T, N), dtype=out_dtype, device=dev)
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     out_scale = 1.0 / K
     op_i8 = i8 or decode  # the decode GEMM takes int8 activation codes
 
@@ -311,7 +313,7 @@ def measure_mlp(args, dev, prerotated: bool = False):
     down = rrs.RRSLinear(Wd, perm_mid)
     del Wg, Wu_, Wd
     stream = torch.cuda.current_stream()
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev)
     h = torch.empty((T, F), dtype=torch.bfloat16, device=dev)
     Y = torch.empty((T, D), dtype=torch.bfloat16, device=dev)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.warmup + args.steps)]
@@ -416,7 +418,7 @@ def run_gpu(args):
                    "out_dtype": args.out_dtype, "note": w.note,
                    "parallelism": f"tp-columns x{world} (W column-sharded, X replicated, NCCL all-gather of Y)"
                    if world > 1 else "single GPU",
-                   "l2": "flushed before every timed step (256 MiB write); per-step CUDA events"},
+                   "l2": L2Flush.describe},
         "tokens_per_s": head["tokens_per_s"],
         "breakdown_ms": head["breakdown_ms"],
         "gemm_tops": head["gemm_tops"],

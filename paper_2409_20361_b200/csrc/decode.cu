@@ -46,11 +46,14 @@ __device__ __forceinline__ void dtrace(int ev, int i) {
     g_dtrace[blockIdx.x][ev][i] = t;
   }
 }
-// experiment knobs of the timeline harness: bit 0 = load X only for the first ring round (W-stream-only timing)
+// experiment knobs of the timeline harness: bit 0 = load X only for the first ring round (W-stream-only timing),
+// bit 1 = issue no MMAs (commits only), bit 2 = converters skip the tcgen05.st, bit 3 = promotion skips the tcgen05.ld
 __device__ int g_dec_exp = 0;
 int g_dec_no_pdl = 0;  // host: launch the GEMM without programmatic dependent launch
+#define RRS_DEXP(bit) (g_dec_exp & (bit))
 #else
 __device__ __forceinline__ void dtrace(int, int) {}
+#define RRS_DEXP(bit) 0
 #endif
 
 namespace dec {
@@ -222,7 +225,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
         const uint64_t xdesc = xdesc0 + (uint64_t)((s * C::X_STAGE) >> 4);
 #pragma unroll
         for (int k = 0; k < KBLK / 32; ++k)
-          ptx::mma_i8_ts(tmem + b * TP, tmem + A_COL0 + a * 32 + k * 8, xdesc + 2 * k, idesc,
+          if (!RRS_DEXP(2)) ptx::mma_i8_ts(tmem + b * TP, tmem + A_COL0 + a * 32 + k * 8, xdesc + 2 * k, idesc,
                          (kin > 0 || k > 0) ? 1u : 0u);
         ptx::mma_commit(&aempty[a]);
         ptx::mma_commit(&xempty[s]);
@@ -271,7 +274,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       }
       ptx::mbar_wait(&aempty[a], ((i / NA) & 1) ^ 1);
       ptx::tc_fence_after();
-      RRS_TMEM_ST32(tmem + lane_off + A_COL0 + a * 32, v);
+      if (!RRS_DEXP(4)) RRS_TMEM_ST32(tmem + lane_off + A_COL0 + a * 32, v);
       prev_a = a;
     }
     if (prev_a >= 0) {
@@ -306,7 +309,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       if (warp == PROM0 && lane == 0) dtrace(4, gl);
       const float sc = s_sm[(gl + rot) % ng] * 0.0625f;  // s_g / 16 (exact: the widened codes are 16 q)
       uint32_t v[TH];
-      if (cols) {
+      if (cols && !RRS_DEXP(8)) {
 #pragma unroll
         for (int c = 0; c < TH / 16; ++c) RRS_TMEM_LD16(tmem + lane_off + b * TP + ch * TH + c * 16, (v + 16 * c));
         RRS_TMEM_WAIT_LD16(v);

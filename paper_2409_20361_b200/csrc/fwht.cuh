@@ -66,7 +66,7 @@ struct FwhtPlan {
 
 // padded shared-memory slot of tile element i (strictly increasing; max < TILE_PAD)
 template <class P>
-RRS_DEVICE int swz(int i) { return i + (i >> 4) + P::PAD_C1 * (i >> P::PAD_S1) + P::PAD_C2 * (i >> P::PAD_S2); }
+RRS_DEVICE constexpr int swz(int i) { return i + (i >> 4) + P::PAD_C1 * (i >> P::PAD_S1) + P::PAD_C2 * (i >> P::PAD_S2); }
 
 // Input widening without F2F (a quarter-rate conversion on sm_100a, 16/clk/SM against 64 DADD/clk/SM:
 // profiles/micro_r2.txt): the f32 bit pattern h of a bf16 value, read as the HIGH word of a double after moving its
@@ -100,7 +100,7 @@ RRS_DEVICE void butterflies(double (&v)[E]) {
 
 // Row-local index of register j = kh*8 + kl of row-thread tp in pass 0.
 template <class P>
-RRS_DEVICE int p0_index(int tp, int j) {
+RRS_DEVICE constexpr int p0_index(int tp, int j) {
   constexpr int per_chunk = P::NP2 / P::E;  // threads per 2^m chunk
   const int a = tp / per_chunk, t = tp % per_chunk;
   return a * P::NP2 + ((j >> 3) << P::HI) + (t << 3) + (j & 7);
@@ -108,7 +108,7 @@ RRS_DEVICE int p0_index(int tp, int j) {
 
 // Row-local index of element k of group u of row-thread tp in the pass over the middle bits [b, b+r).
 template <class P, int b, int r>
-RRS_DEVICE int p2_index(int tp, int u, int k) {
+RRS_DEVICE constexpr int p2_index(int tp, int u, int k) {
   const int g = tp + P::TP2 * u;  // the other bits, in [0, K / 2^r)
   return (g & ((1 << b) - 1)) | (k << b) | ((g >> b) << (b + r));
 }
@@ -168,7 +168,7 @@ RRS_DEVICE void h28_lean(double (&v)[E], Emit&& emit) {
 // (L = b), or the H28 pass (L = -2).
 
 template <class P, int L>
-RRS_DEVICE int reg_index(int tp, int j) {
+RRS_DEVICE constexpr int reg_index(int tp, int j) {
   if constexpr (L == -1) {
     return p0_index<P>(tp, j);
   } else if constexpr (L == -2) {
@@ -180,18 +180,39 @@ RRS_DEVICE int reg_index(int tp, int j) {
   }
 }
 
+// In the pass-0 and H28 layouts of every plan, and in every layout of the 2^m plans, the tile index splits into disjoint
+// bit fields: the row and thread part reg_index(tp, 0) and the register part reg_index(0, j)
+// (tests/test_fwht_layout_cpu.py).  Disjoint fields add without carries, so every shift in swz distributes over them:
+// swz(rr K + reg_index(tp, j)) = swz(rr K + reg_index(tp, 0)) + swz(reg_index(0, j)) -- one base address per pass and a
+// compile-time offset per register.  (The middle passes of 28 * 2^m plans, whose thread count 16 * 28 is not a power of
+// two, compute each address.)
+template <class P, int L>
+__host__ __device__ constexpr bool separable() { return P::kPow2 || L < 0; }
+
 template <class P, int L>
 RRS_DEVICE void store_layout(double* sm, int rr, int tp, const double (&v)[P::E]) {
   constexpr int n = (L == -2) ? 28 : P::E;
+  if constexpr (separable<P, L>()) {
+    double* base = sm + swz<P>(rr * P::K + reg_index<P, L>(tp, 0));
 #pragma unroll
-  for (int j = 0; j < n; ++j) sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))] = v[j];
+    for (int j = 0; j < n; ++j) base[swz<P>(reg_index<P, L>(0, j))] = v[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < n; ++j) sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))] = v[j];
+  }
 }
 
 template <class P, int L>
 RRS_DEVICE void load_layout(const double* sm, int rr, int tp, double (&v)[P::E]) {
   constexpr int n = (L == -2) ? 28 : P::E;
+  if constexpr (separable<P, L>()) {
+    const double* base = sm + swz<P>(rr * P::K + reg_index<P, L>(tp, 0));
 #pragma unroll
-  for (int j = 0; j < n; ++j) v[j] = sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))];
+    for (int j = 0; j < n; ++j) v[j] = base[swz<P>(reg_index<P, L>(0, j))];
+  } else {
+#pragma unroll
+    for (int j = 0; j < n; ++j) v[j] = sm[swz<P>(rr * P::K + reg_index<P, L>(tp, j))];
+  }
 }
 
 // The middle passes [b, HI) following a pass with layout PL; finally the H28 pass.  Ends with v in the
@@ -285,7 +306,7 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], 
 }
 
 template <class P>
-RRS_DEVICE int out_col(int tp, int j) {
+RRS_DEVICE constexpr int out_col(int tp, int j) {
   return reg_index<P, last_layout<P>()>(tp, j);
 }
 

@@ -103,10 +103,10 @@ RRS_DEVICE void fwht_phase(const uint16_t* __restrict__ X, int64_t T, unsigned* 
     tile_coords<P>((int)threadIdx.x, rr0, tp0);
     const int64_t row = tile * P::R + rr0;
     const bool live = act && row < T;
-    float* xr = Xr + (live ? row : 0) * (int64_t)K;
+    float* xr = Xr + (live ? row : 0) * (int64_t)K + out_col<P>(tp0, 0);  // + a compile-time offset per register
     auto emit = [&](int j, float f) {
       cm[j] = live ? fmaxf(cm[j], fabsf(f)) : cm[j];
-      if (live) xr[out_col<P>(tp0, j)] = f;
+      if (live) xr[out_col<P>(0, j)] = f;
     };
     fwht_tile<P>(stage + buf * P::TILE, sm, v, rr, tp, emit);  // ends with __syncthreads: stage[buf] is free
     trace(0, 2 + 2 * (it < 5 ? it : 5));
@@ -232,8 +232,9 @@ RRS_DEVICE void write_codes(const float (&z)[32], float m, int64_t trow, int K, 
     for (int k = 0; k < 32; k += 4) {
       float q[4];
 #pragma unroll
-      for (int h = 0; h < 4; ++h)  // R10, R11; "+ 0" turns rint's -0 into the canonical +0 (code byte 0x00)
-        q[h] = __fadd_rn(fminf(fmaxf(rintf(__fmul_rn(z[k + h], r)), -8.0f), 7.0f), 0.0f);
+      for (int h = 0; h < 4; ++h)  // R10; "+ 0" turns rint's -0 into the canonical +0 (code byte 0x00).  The R11 clamp
+        // never binds here: |z| <= m, so |fl(z fl(7/m))| <= 7 (1 + 2^-24)^2 < 7.5 and rint gives |q| <= 7
+        q[h] = __fadd_rn(rintf(__fmul_rn(z[k + h], r)), 0.0f);
       uint32_t lo, hi;
       asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
           : "=r"(lo) : "f"(q[1]), "f"(q[0]));
@@ -438,7 +439,10 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   for (int ch = 0; ch < CH; ++ch) gm[ch] = 0.0f;
   int rf, tf;  // (tile row, row-thread) of this thread in the FWHT's last layout
   tile_coords<P>(tid, rf, tf);
-  float* xs_row = xs + rf * S::KP;
+  // the X~ stores: out_col(tf, j) = out_col(tf, 0) + out_col(0, j) in disjoint bits (fwht.cuh), so the padded address
+  // c + c/32 is a per-thread base plus a compile-time offset per register
+  const int c0 = out_col<P>(tf, 0);
+  float* xs_row = xs + rf * S::KP + c0 + (c0 >> 5);
   int64_t cur = blockIdx.x, nxt = ntiles;  // (thread 0) this tile and the claimed next one
   if (tid == 0 && cur < ntiles) nxt = dyn ? gridDim.x + (int64_t)atomicAdd(&gbar[2], 1u) : cur + gridDim.x;
   int ntl = 0;
@@ -458,7 +462,7 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
       int rr_, tp_;
       fwht_tile<P>(stage, sm, v, rr_, tp_,
                    [&](int j, float f) {
-                     const int c = out_col<P>(tf, j);
+                     const int c = out_col<P>(0, j);
                      xs_row[c + (c >> 5)] = f;
                    },
                    [&] { if (tid == 0 && nxt < ntiles) issue(nxt); });

@@ -1,7 +1,8 @@
 // Timeline of the decode regime at configs[3] (K = N = 8192), synthetic codes: rrs_decode_gemm_kernel (CTAs 0..7) alone,
 // or the whole layer (prologue_decode_group_kernel + the GEMM launched with PDL, as rrs_linear does).
 //   tools/build_traces.sh;  tools/decode_trace T [mode]   mode: 0 GEMM, 1 GEMM with X loaded once (W stream only),
-//                                                          2 layer (prologue + GEMM), 3 layer without PDL
+//                                                          2 layer (prologue + GEMM), 3 layer without PDL,
+//                                                          4-7: mode 1 and no MMA / no TMEM store / no TMEM load / none
 #include <cstdio>
 #include <vector>
 #include <algorithm>
@@ -32,7 +33,9 @@ int main(int argc, char** argv) {
   }
   cudaMemcpy(perm, hp.data(), K * 4, cudaMemcpyHostToDevice);
   int exp = mode == 1 ? 1 : 0;
+  if (mode >= 4) exp = 1 | (mode == 4 ? 2 : mode == 5 ? 4 : mode == 6 ? 8 : 14);  // 4 no MMA, 5 no st, 6 no ld, 7 none
   rrs::g_dec_no_pdl = mode == 3;
+  const bool layer = mode == 2 || mode == 3;
   cudaMemcpyToSymbol(rrs::g_dec_exp, &exp, sizeof(int));
   rrs::DecodeArgs a{X, xs, sg, W, ws, T, N, K, 128, 1.0f / K, Y, 0, N};
   for (int rep = 0; rep < 4; ++rep) {
@@ -41,7 +44,7 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
     cudaError_t e = cudaSuccess;
-    if (mode >= 2)
+    if (layer)
       e = rrs::launch_prologue_decode(Xb, T, K, perm, nullptr, nullptr, sg, nullptr, X, xs, false, 128, 0);
     if (e == cudaSuccess) e = rrs::launch_decode_gemm(a, nsm, 0);
     cudaEventRecord(e1);
@@ -55,7 +58,7 @@ int main(int argc, char** argv) {
   static unsigned long long hp2[3][1024][16];
   rrs::copy_prologue_trace(hp2, sizeof(hp2));
   unsigned long long t0 = h[0][5][0];
-  if (mode >= 2) {  // common origin: the first prologue CTA's start
+  if (layer) {  // common origin: the first prologue CTA's start
     for (int c = 0; c < T && c < 1024; ++c) if (hp2[2][c][0] && hp2[2][c][0] < t0) t0 = hp2[2][c][0];
     for (int sl = 0; sl < 7; ++sl) {
       double mn = 1e30, mx = -1e30;

@@ -12,6 +12,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2409_20361_b200 as rrs  # noqa: E402
 from rrs_synth import WORKLOADS, make_layer  # noqa: E402
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench"))
+from l2flush import L2Flush  # noqa: E402  (bench/l2flush.py)
 
 
 def dev_bf16(b):
@@ -39,7 +41,7 @@ def main():
     X_bits, W_bits, Xc = make_layer(w, index=list(WORKLOADS).index("c4_decode_t64"))
     perm = rrs.calibrate_perm(dev_bf16(Xc))
     layer = rrs.RRSLinear(dev_bf16(W_bits), perm, decode=True)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush("cuda")
     K, N = w.K, w.N
     for T in Ts:
         X = dev_bf16(X_bits[:T])

@@ -13,6 +13,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2409_20361_b200 as rrs  # noqa: E402
 from rrs_synth import WORKLOADS, make_layer  # noqa: E402
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench"))
+from l2flush import L2Flush  # noqa: E402  (bench/l2flush.py)
 
 
 def dev_bf16(b):
@@ -22,7 +24,7 @@ def dev_bf16(b):
 def main():
     names = sys.argv[1:] or ["c2_llama2_7b_qo", "c3_llama3_8b_up", "c5_llama3_70b_up_rank8", "c3_llama3_8b_down",
                              "c4_decode_t64", "c4_decode_t1"]
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = L2Flush("cuda")
     for name in names:
         w = WORKLOADS[name]
         X_bits, _, Xc = make_layer(w, index=list(WORKLOADS).index(name), N=8)
