@@ -14,16 +14,13 @@
 //     chunk j0..j0+31, byte b (0..15) = (q[j0+b] << 4) | (q[j0+16+b] & 0xF).  Widening is then two masks per
 //     32-bit word: (w & 0xF0F0F0F0) holds 16 q[j0+4i..] as int8 bytes, ((w << 4) & 0xF0F0F0F0) holds 16 q[j0+16+4i..],
 //     i.e. the MMA sums 16 P_g exactly (|16 P_g| <= 16 * 6272 < 2^17) and the promotion scale is s_g / 16;
-//   * each CTA owns 128 W rows (one M = 128 block: half of a 256-row decode4 tile, a contiguous 8 KiB per K-block)
-//     and a contiguous range of K-blocks; the S CTAs (a pair at configs[3]) that split a row block's K form a
-//     cluster and reduce their f32 partials through DSMEM in a fixed rank order (deterministic, R15) -- no global
-//     scratch, no memset, no second kernel;
+//   * each CTA owns 256 W rows (two M = 128 halves sharing every X tile) and a contiguous range of K-blocks;
+//     the S CTAs that split a row block's K form a cluster and reduce their f32 partials through DSMEM in a
+//     fixed rank order (deterministic, R15) -- no global scratch, no memset, no second kernel;
 //   * the W ring starts filling BEFORE griddepcontrol.wait (W does not depend on the prologue), so with
-//     programmatic dependent launch the W stream overlaps the prologue's tail; the X ring (8-16 stages) is issued
-//     as deep as shared memory allows, so no X load latency sits in the per-K-block loop.
-// Warps: 0 W producer, 1 TMEM allocator + single-thread MMA issuer, 2-9 converters (W nibbles -> TMEM; two sets of
-// four lane quadrants take alternate K-blocks), 10-13 promotion (TMEM P_g -> registers, acc += s_g P_g) + epilogue,
-// 14 X producer.
+//     programmatic dependent launch the W stream overlaps the prologue's tail.
+// Warps: 0 TMA producer, 1 TMEM allocator + single-thread MMA issuer, 2-5 converters (W nibbles -> TMEM),
+// 6-13 promotion (TMEM P_g -> registers, acc += s_g P_g) + epilogue.
 #include <algorithm>
 #include <cstring>
 #include <cuda.h>
@@ -46,42 +43,36 @@ __device__ __forceinline__ void dtrace(int ev, int i) {
     g_dtrace[blockIdx.x][ev][i] = t;
   }
 }
-// experiment knobs of the timeline harness: bit 0 = load X only for the first ring round (W-stream-only timing),
-// bit 1 = issue no MMAs (commits only), bit 2 = converters skip the tcgen05.st, bit 3 = promotion skips the tcgen05.ld
+// experiment knobs of the timeline harness: bit 0 = load X only for the first ring round (W-stream-only timing)
 __device__ int g_dec_exp = 0;
 int g_dec_no_pdl = 0;  // host: launch the GEMM without programmatic dependent launch
-#define RRS_DEXP(bit) (g_dec_exp & (bit))
 #else
 __device__ __forceinline__ void dtrace(int, int) {}
-#define RRS_DEXP(bit) 0
 #endif
 
 namespace dec {
-constexpr int min_i(int a, int b) { return a < b ? a : b; }
-constexpr int ROWS = 128;                // W rows per CTA: one MMA M = 128 block
+constexpr int ROWS = 256;                // W rows per CTA (two MMA halves of 128)
 constexpr int KBLK = 128;                // codes per K-block
-constexpr int TILE4 = 256 * KBLK / 2;    // one decode4 tile in HBM (256 rows x one K-block, 16 KiB)
-constexpr int W_STAGE = ROWS * KBLK / 2; // this CTA's half of a tile: 8 KiB, contiguous (rows at 64 bytes)
-constexpr int NS = 16;                   // W ring stages (128 KiB in flight)
-constexpr int NA = 8;                    // TMEM A stages (widened W): 8 K-blocks between conversion and MMA
-constexpr int NACC = 4;                  // TMEM accumulator buffers (groups in flight between MMA and promotion)
-constexpr int NCONV = 8, NPROM = 8;      // two converter sets (even / odd K-blocks) x 4 lane quadrants; promotion:
-                                         // 4 lane quadrants x 2 column halves
+constexpr int W_STAGE = ROWS * KBLK / 2; // packed W bytes per K-block: one contiguous 16 KiB tile
+constexpr int NS = 8;                    // W ring stages
+constexpr int min_i(int a, int b) { return a < b ? a : b; }
+constexpr int NA = 3;                    // TMEM A stages (widened W)
+constexpr int NCONV = 4, NPROM = 8;
 constexpr int W_PROD = 0, MMA_WARP = 1, CONV0 = 2, PROM0 = CONV0 + NCONV, X_PROD = PROM0 + NPROM;
 constexpr int THREADS = (X_PROD + 1) * 32;
-constexpr int A_COL0 = 256;              // TMEM columns [256, 256 + 32 NA): A stages; [0, NACC TP): accumulators
-constexpr int TMEM_COLS = 512;
+constexpr int A_COL0 = 256;              // TMEM columns [256, 256 + 64 NA): A stages; [0, 4 TP): accumulators
 constexpr int MAX_G = 160;
 
 template <int TP>
 struct Cfg {
   static constexpr int X_STAGE = TP * KBLK;   // int8 X codes per K-block (SWIZZLE_128B tile)
-  static constexpr int NX = min_i(16, 65536 / X_STAGE);  // X ring: 8 stages at TP = 64, 16 below
+  static constexpr int NX = min_i(16, 65536 / X_STAGE);  // X ring: 8 stages at TP = 64, 16 below (X loads are L2 hits
+                                                         // whose latency must not sit in the per-K-block loop)
   static constexpr int X_OFF = NS * W_STAGE;
   static constexpr int RING = X_OFF + NX * X_STAGE;
   static constexpr int ROWB = (TP + 4) * 4;      // one row of partials (f32, 16-byte aligned stride)
-  // after the K loop, on the ring: this CTA's partials [128][TP + 4] f32, then the S incoming slots
-  // [S][128/S][TP + 4] (the same 128 rows' worth of bytes)
+  // after the K loop, on the ring: this CTA's partials [256][TP + 4] f32, then the S incoming slots
+  // [S][256/S][TP + 4] (the same 256 rows' worth of bytes)
   static constexpr int RED = 2 * ROWS * ROWB;
   static constexpr int SMEM = 1024 + RING + 1024 + MAX_G * 4 + 64 * 4 + ROWS * 4;  // + s_g, alpha_t, beta_n
   static_assert(X_STAGE % 1024 == 0 && W_STAGE % 1024 == 0, "1024-byte aligned swizzle atoms");
@@ -113,7 +104,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   constexpr int NX = C::NX;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* wring = smem;                                  // [NS][8 KiB] packed W half-tiles
+  uint8_t* wring = smem;                                  // [NS][16 KiB] packed W tiles
   uint8_t* xring = smem + C::X_OFF;                       // [NX][TP x 128] int8 X codes
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::RING);
   uint64_t* wfull = bars;
@@ -123,20 +114,20 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   uint64_t* afull = xempty + NX;
   uint64_t* aempty = afull + NA;
   uint64_t* tfull = aempty + NA;
-  uint64_t* tempty = tfull + NACC;
-  uint64_t* redbar = tempty + NACC;     // the peers' partial slices have landed (bulk copies, complete_tx)
+  uint64_t* tempty = tfull + 2;
+  uint64_t* redbar = tempty + 2;     // the peers' partial slices have landed (bulk copies, complete_tx)
   uint32_t* taddr_slot = reinterpret_cast<uint32_t*>(redbar + 1);
   float* s_sm = reinterpret_cast<float*>(smem + C::RING + 1024);
   float* xs_sm = s_sm + MAX_G;   // alpha_t * out_scale, t < T
-  float* ws_sm = xs_sm + 64;     // beta_n of this CTA's 128 rows (0 past N)
-  float* part = reinterpret_cast<float*>(wring);          // after the K loop: own partials [128][TP + 4]
-  float* slots = part + ROWS * (TP + 4);                   // incoming [S][128/S][TP + 4]
+  float* ws_sm = xs_sm + 64;     // beta_n of this CTA's 256 rows (0 past N)
+  float* part = reinterpret_cast<float*>(wring);          // after the K loop: own partials [256][TP + 4]
+  float* slots = part + ROWS * (TP + 4);                   // incoming [S][256/S][TP + 4]
 
   const uint32_t warp = ptx::warp_idx();
   const int lane = threadIdx.x & 31;
   const int S = p.S;
   const uint32_t rank = S > 1 ? ptx::cluster_ctarank() : 0u;
-  const int rb = blockIdx.x / S;      // 128-row block = half (rb & 1) of decode4 tile row (rb >> 1)
+  const int rb = blockIdx.x / S;
   const int row0 = rb * ROWS;
   const int nkb = p.kb_per_cta;
   const int kb0 = (int)rank * nkb;
@@ -144,27 +135,26 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   const int g0 = kb0 / p.gpb;
   const int rows_per = ROWS / S;
   // every row block walks its K range starting at a different group (rotated by the row block): the X tiles are shared
-  // by all row blocks, and 64 CTAs requesting the same 8 KiB at the same moment serialise on its L2 lines (measured:
-  // 2.4 us per X load).  The group order of the promotion differs per row block but is fixed (R15).
+  // by all row blocks, and CTAs requesting the same X tile at the same moment serialise on its L2 lines.  The group
+  // order of the promotion differs per row block but is fixed (R15).
   const int rot = rb % ng;
   auto kb_at = [&](int i) { return ((i / p.gpb + rot) % ng) * p.gpb + i % p.gpb; };  // loop index -> K-block (CTA range)
 
-  static_assert(NX <= 16 && NS <= 16, "barrier area");
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tmap_x);
     for (int s = 0; s < NS; ++s) {
       ptx::mbar_init(&wfull[s], 1);
-      ptx::mbar_init(&wempty[s], 4);
+      ptx::mbar_init(&wempty[s], NCONV);
     }
     for (int s = 0; s < NX; ++s) {
       ptx::mbar_init(&xfull[s], 1);
       ptx::mbar_init(&xempty[s], 1);
     }
     for (int a = 0; a < NA; ++a) {
-      ptx::mbar_init(&afull[a], 4);
+      ptx::mbar_init(&afull[a], NCONV);
       ptx::mbar_init(&aempty[a], 1);
     }
-    for (int b = 0; b < NACC; ++b) {
+    for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
       ptx::mbar_init(&tempty[b], NPROM);
     }
@@ -172,22 +162,22 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     ptx::fence_barrier_init();
   }
   if (threadIdx.x == 0) dtrace(5, 0);
-  if (warp == MMA_WARP) ptx::tmem_alloc(taddr_slot, TMEM_COLS);
+  if (warp == MMA_WARP) ptx::tmem_alloc(taddr_slot, 512);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *taddr_slot;
 
   if (warp == W_PROD) {
-    // ------------------------------------------------------------------ W stream: one 8 KiB bulk copy per K-block
+    // ------------------------------------------------------------------ W stream: one 16 KiB bulk copy per K-block
     // (W does not depend on the prologue: no griddepcontrol.wait, the ring fills while the prologue finishes)
     if (ptx::elect_one()) {
-      const uint8_t* wsrc = p.Wp4 + ((int64_t)(rb >> 1) * (p.K / KBLK) + kb0) * TILE4 + (rb & 1) * W_STAGE;
+      const uint8_t* wsrc = p.Wp4 + ((int64_t)rb * (p.K / KBLK) + kb0) * W_STAGE;
       for (int i = 0; i < nkb; ++i) {
         const int s = i % NS;
         ptx::mbar_wait(&wempty[s], ((i / NS) & 1) ^ 1);
         ptx::mbar_arrive_expect_tx(&wfull[s], W_STAGE);
-        ptx::bulk_load(wring + s * W_STAGE, wsrc + (int64_t)kb_at(i) * TILE4, W_STAGE, &wfull[s]);
+        ptx::bulk_load(wring + s * W_STAGE, wsrc + (int64_t)kb_at(i) * W_STAGE, W_STAGE, &wfull[s]);
         dtrace(0, i);
       }
     }
@@ -217,16 +207,18 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
       for (int i = 0; i < nkb; ++i) {
         const int s = i % NX, a = i % NA;
         const int gl = i / p.gpb, kin = i % p.gpb;
-        const uint32_t b = gl % NACC;
-        if (kin == 0) ptx::mbar_wait(&tempty[b], ((gl / NACC) & 1) ^ 1);
+        const uint32_t b = gl & 1;
+        if (kin == 0) ptx::mbar_wait(&tempty[b], ((gl >> 1) & 1) ^ 1);
         ptx::mbar_wait(&afull[a], (i / NA) & 1);
         ptx::mbar_wait(&xfull[s], (i / NX) & 1);
         ptx::tc_fence_after();
         const uint64_t xdesc = xdesc0 + (uint64_t)((s * C::X_STAGE) >> 4);
 #pragma unroll
-        for (int k = 0; k < KBLK / 32; ++k)
-          if (!RRS_DEXP(2)) ptx::mma_i8_ts(tmem + b * TP, tmem + A_COL0 + a * 32 + k * 8, xdesc + 2 * k, idesc,
-                         (kin > 0 || k > 0) ? 1u : 0u);
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int k = 0; k < KBLK / 32; ++k)
+            ptx::mma_i8_ts(tmem + b * (2 * TP) + h * TP, tmem + A_COL0 + a * 64 + h * 32 + k * 8, xdesc + 2 * k, idesc,
+                           (kin > 0 || k > 0) ? 1u : 0u);
         ptx::mma_commit(&aempty[a]);
         ptx::mma_commit(&xempty[s]);
         if (kin == p.gpb - 1) ptx::mma_commit(&tfull[b]);
@@ -236,92 +228,78 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     __syncwarp();
   } else if (warp < PROM0) {
     // ------------------------------------------------------------------ converters: packed W -> int8 in TMEM
-    // set 0 takes the even K-blocks, set 1 the odd ones (two tiles in conversion at once); a warp may only access
-    // the TMEM lane quadrant warp % 4, and row r of the half-tile is TMEM lane r
-    const int q = warp & 3, set = (int)(warp - CONV0) >> 2;
+    const int q = warp & 3;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-    const int r = q * 32 + lane;
-    // software-pipelined: the tcgen05.st of tile i completes (wait::st, then afull) only after tile i + 2 has been read
-    // and widened, so the store's latency overlaps the next tile's shared-memory loads and ALU work
-    int prev_a = -1;
-    for (int i = set; i < nkb; i += 2) {
+    for (int i = 0; i < nkb; ++i) {
       const int s = i % NS, a = i % NA;
       ptx::mbar_wait(&wfull[s], (i / NS) & 1);
-      // the tile is stored pre-swizzled: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3), so every
-      // quarter-warp's 16-byte loads hit 8 distinct bank groups (r and the tile row differ by a multiple of 128)
-      const uint8_t* rowp = wring + s * W_STAGE + r * 64;
-      uint32_t v[32];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        const uint4 w = *reinterpret_cast<const uint4*>(rowp + ((c ^ ((r >> 1) & 3)) << 4));
-        const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          v[8 * c + j] = ww[j] & 0xF0F0F0F0u;             // 16 q[j0 + 4j ..]     (high nibbles)
-          v[8 * c + 4 + j] = (ww[j] << 4) & 0xF0F0F0F0u;  // 16 q[j0 + 16 + 4j ..] (low nibbles)
-        }
-      }
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&wempty[s]);  // the W stage is in registers: the producer may refill it
-      if (prev_a >= 0) {  // the previous tile's store has had this tile's loads to complete
-        ptx::tmem_st_wait();
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          ptx::mbar_arrive(&afull[prev_a]);
-          if (warp == CONV0) dtrace(2, i - 2);
-        }
-      }
       ptx::mbar_wait(&aempty[a], ((i / NA) & 1) ^ 1);
       ptx::tc_fence_after();
-      if (!RRS_DEXP(4)) RRS_TMEM_ST32(tmem + lane_off + A_COL0 + a * 32, v);
-      prev_a = a;
-    }
-    if (prev_a >= 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = h * 128 + q * 32 + lane;
+        // the tile is stored pre-swizzled: 16-byte chunk c of row r sits at chunk c ^ ((r >> 1) & 3), so every
+        // quarter-warp's 16-byte loads hit 8 distinct bank groups
+        const uint8_t* rowp = wring + s * W_STAGE + r * 64;
+        uint32_t v[32];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 w = *reinterpret_cast<const uint4*>(rowp + ((c ^ ((r >> 1) & 3)) << 4));
+          const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            v[8 * c + j] = ww[j] & 0xF0F0F0F0u;             // 16 q[j0 + 4j ..]     (high nibbles)
+            v[8 * c + 4 + j] = (ww[j] << 4) & 0xF0F0F0F0u;  // 16 q[j0 + 16 + 4j ..] (low nibbles)
+          }
+        }
+        RRS_TMEM_ST32(tmem + lane_off + A_COL0 + a * 64 + h * 32, v);
+      }
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&afull[prev_a]);
+      if (lane == 0) {
+        ptx::mbar_arrive(&wempty[s]);
+        ptx::mbar_arrive(&afull[a]);
+        if (warp == CONV0) dtrace(2, i);
+      }
     }
-  } else if (warp < X_PROD) {
+  } else {
     // ------------------------------------------------------------------ promotion
-    // warp = lane quadrant q (warp % 4) x column half ch: TP / 2 token columns of 32 W rows; all its TMEM loads of a
-    // group are issued before one wait (the loads' latency, not their bandwidth, paced the MMA with two buffers)
-    constexpr int TH = TP / 2 < 16 ? 16 : TP / 2;  // columns per warp (TP = 16: the second half has none)
-    const int q = warp & 3, ch = (int)(warp - PROM0) >> 2;
-    const bool cols = ch * TH < TP;
+    const int q = warp & 3, h = (warp - PROM0) >> 2;
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     ptx::pdl_wait();  // s_g come from the prologue
     for (int g = threadIdx.x - PROM0 * 32; g < ng; g += NPROM * 32) s_sm[g] = p.s_group[g0 + g];
     {  // the epilogue's scales, read once here (off the critical path)
       const int i = threadIdx.x - PROM0 * 32;  // 0 .. 255
       if (i < p.T) xs_sm[i] = p.x_scale[i] * p.out_scale;
-      if (i < ROWS) ws_sm[i] = row0 + i < p.N ? p.w_scale[row0 + i] : 0.0f;
+      ws_sm[i] = row0 + i < p.N ? p.w_scale[row0 + i] : 0.0f;
     }
     asm volatile("bar.sync 1, %0;" ::"n"(NPROM * 32));
-    float acc[TH];  // sum_g s_g P_g of this thread's W row for this warp's token columns
+    float acc[TP];  // sum_g s_g P_g of this thread's W row for the TP token columns
 #pragma unroll
-    for (int t = 0; t < TH; ++t) acc[t] = 0.0f;
+    for (int t = 0; t < TP; ++t) acc[t] = 0.0f;
     for (int gl = 0; gl < ng; ++gl) {
-      const uint32_t b = gl % NACC;
-      ptx::mbar_wait(&tfull[b], (gl / NACC) & 1);
+      const uint32_t b = gl & 1;
+      ptx::mbar_wait(&tfull[b], (gl >> 1) & 1);
       ptx::tc_fence_after();
       if (warp == PROM0 && lane == 0) dtrace(4, gl);
       const float sc = s_sm[(gl + rot) % ng] * 0.0625f;  // s_g / 16 (exact: the widened codes are 16 q)
-      uint32_t v[TH];
-      if (cols && !RRS_DEXP(8)) {
+      // the group's loads two at a time, one wait per pair (the load latency, not its bandwidth, paced the MMA)
 #pragma unroll
-        for (int c = 0; c < TH / 16; ++c) RRS_TMEM_LD16(tmem + lane_off + b * TP + ch * TH + c * 16, (v + 16 * c));
+      for (int c = 0; c < TP / 16; c += 2) {
+        uint32_t v[32];
+        RRS_TMEM_LD16(tmem + lane_off + b * (2 * TP) + h * TP + c * 16, v);
+        if (c + 1 < TP / 16) RRS_TMEM_LD16(tmem + lane_off + b * (2 * TP) + h * TP + (c + 1) * 16, (v + 16));
         RRS_TMEM_WAIT_LD16(v);
+        if (c + 1 < TP / 16) RRS_REG_FENCE16((v + 16));
+        if (c + 2 >= TP / 16) {
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(&tempty[b]);
+        }
 #pragma unroll
-        for (int c = 1; c < TH / 16; ++c) RRS_REG_FENCE16((v + 16 * c));
-      }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[b]);
-      if (cols) {
-#pragma unroll
-        for (int j = 0; j < TH; ++j) acc[j] = fmaf(sc, (float)(int)v[j], acc[j]);
+        for (int j = 0; j < 32; ++j)
+          if (c * 16 + j < TP) acc[c * 16 + j] = fmaf(sc, (float)(int)v[j], acc[c * 16 + j]);
       }
     }
     // every MMA has completed (this warp saw the last tfull), so every converter and every ring stage of this CTA
@@ -329,14 +307,12 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
     // (16-byte stores, row stride TP + 4 floats) and a proxy fence makes them visible to the bulk copies
     if (warp == PROM0 && lane == 0) dtrace(7, 0);
     asm volatile("barrier.sync 2, %0;" ::"n"(THREADS) : "memory");
-    const int r = q * 32 + lane;
-    if (cols) {
+    const int r = h * 128 + q * 32 + lane;
 #pragma unroll
-      for (int t4 = 0; t4 < TH / 4; ++t4)
-        if (ch * TH + 4 * t4 < p.T)
-          *reinterpret_cast<float4*>(part + r * (TP + 4) + ch * TH + 4 * t4) =
-              make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
-    }
+    for (int t4 = 0; t4 < TP / 4; ++t4)
+      if (4 * t4 < p.T)
+        *reinterpret_cast<float4*>(part + r * (TP + 4) + 4 * t4) =
+            make_float4(acc[4 * t4], acc[4 * t4 + 1], acc[4 * t4 + 2], acc[4 * t4 + 3]);
     ptx::fence_proxy_async_shared();
   }
   // the other warps' arrival at that CTA barrier (non-aligned form: producer lanes may still be diverged)
@@ -347,7 +323,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   if (S > 1) ptx::cluster_sync();
   else __syncthreads();
   if (warp == PROM0 && lane == 0) dtrace(7, 1);
-  // the owner of rows [r 128/S, (r+1) 128/S) is rank r: one bulk copy (TMA) per peer of that contiguous slice into the
+  // the owner of rows [r 256/S, (r+1) 256/S) is rank r: one bulk copy (TMA) per peer of that contiguous slice into the
   // peer's slot [my rank], completing on the peer's redbar -- shared-memory-to-shared-memory over the cluster
   const uint32_t slice_bytes = (uint32_t)(rows_per * (TP + 4) * 4);
   if (threadIdx.x == 0 && S > 1) {
@@ -365,7 +341,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   __syncthreads();  // (already implied by the cluster barrier above; stated for the shared-memory race checker)
   if (threadIdx.x == 0) dtrace(7, 2);
   // ---- fixed-order reduction over the S slots (ranks 0..S-1) and the epilogue: rank r writes rows
-  // [r 128/S, (r+1) 128/S) of the row block
+  // [r 256/S, (r+1) 256/S) of the row block
   {
     const int nout = ((p.T + 3) / 4) * rows_per;  // (4 tokens, 1 row) per item
     for (int idx = threadIdx.x; idx < nout; idx += THREADS) {
@@ -398,7 +374,7 @@ rrs_decode_gemm_kernel(const __grid_constant__ CUtensorMap tmap_x, DecodeParams 
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
-  if (warp == MMA_WARP) ptx::tmem_dealloc(tmem, TMEM_COLS);
+  if (warp == MMA_WARP) ptx::tmem_dealloc(tmem, 512);
 }
 
 // ------------------------------------------------------------------------------------ host side
@@ -464,7 +440,7 @@ cudaError_t launch_decode_gemm(const DecodeArgs& a, int nsm, cudaStream_t st) {
   if (!decode_gemm_supports(a.T, a.K, a.group)) return cudaErrorInvalidValue;
   const int KBt = (int)(a.K / KBLK), G = (int)(a.K / a.group), gpb = a.group / KBLK;
   const int R = (int)((a.N + ROWS - 1) / ROWS);
-  // 128-row blocks; split K over a cluster of S CTAs (whole groups each) while the grid still fits on the SMs
+  // split K over a cluster of S CTAs (whole groups each) while the grid still fits on the SMs
   int S = 1;
   for (int s : {2, 4, 8})
     if (G % s == 0 && (int64_t)R * s <= nsm) S = s;

@@ -345,9 +345,12 @@ static unsigned next_slot() {
 }
 
 // FWHT plan of the fused kernel: 64 doubles per thread (one transpose per row at K = 4096) where the plan exists
+#ifndef RRS_GROUP_B6_MIN_K  // (timeline harness: -DRRS_GROUP_B6_MIN_K=1<<30 builds the 32-double plans everywhere)
+#define RRS_GROUP_B6_MIN_K 4096
+#endif
 template <int K>
 struct GroupPlan {
-  using P = FwhtPlan<K, (K >= 4096 ? 6 : 5)>;
+  using P = FwhtPlan<K, (K >= RRS_GROUP_B6_MIN_K ? 6 : 5)>;
 };
 
 template <int K>

@@ -10,3 +10,4 @@ L="-lcuda -L$NL -l:libnccl.so.2 -Xlinker -rpath=$NL"
 nvcc $F -o $R/tools/decode_trace $R/tools/decode_trace.cu $C/api.cu $C/prologue.cu $C/gemm.cu $L &
 nvcc $F -o $R/bench/micro/prologue_trace $R/bench/micro/prologue_trace.cu $C/api.cu $C/gemm.cu $C/decode.cu $L &
 wait
+nvcc $F -DRRS_GROUP_B6_MIN_K=1073741824 -o $R/bench/micro/prologue_trace_b5 $R/bench/micro/prologue_trace.cu $C/api.cu $C/gemm.cu $C/decode.cu $L
