@@ -318,7 +318,9 @@ static rrs_status prologue(const void* X, int64_t T, int64_t K, const int32_t* p
   // prefill, K = 2^m: one cooperative launch that reduces group maxima only (s_g needs no per-channel c_j); a caller
   // that wants chan_max, or a grid that cannot be co-resident, takes the two-kernel prologue below
   cudaError_t e = cudaSuccess;
-  if (T > 0 && !want_chan_max && rrs::prologue_fused_supports_k(K)) {
+  // (only while X~ stays L2-resident: at 8192 x 8192 the fused kernel's second pass re-reads 268 MB from HBM and the
+  // two-kernel path, which streams it once in a pass sized for that, is faster: 218 vs 258 us, profiles/time_prologue)
+  if (T > 0 && !want_chan_max && rrs::prologue_fused_supports_k(K) && T * K * 4 <= (int64_t(80) << 20)) {
     e = rrs::launch_prologue_fused(static_cast<const uint16_t*>(X), T, K, Xr, perm, s_group, Xq, Xq8, x_scale, e4m3,
                                    group, st);
     if (e == cudaSuccess) return RRS_OK;
