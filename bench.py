@@ -434,13 +434,15 @@ def run_gpu(args):
                      "tcgen05_microbench_peak": micro_peak,
                      "frac_vs_nominal_4500": head["gemm_tops"] / 4500.0,
                      "algorithmic": "2*T*K*N_local int ops per launch / rrs_gemm CUDA-event time (SURVEY 8(d))"},
-        "prologue_roofline": {"bound": "fp64", "kernel": "prologue_fused_kernel" if pow2 else
+        "prologue_roofline": {"bound": "fp64", "kernel": "prologue_group_kernel" if pow2 else
                               "fwht_colmax_kernel + smooth_quant_kernel",
                               "achieved": dadd / t_pro / 1e12, "peak": fp64_peak / 1e12, "unit": "T DADD/s",
                               "frac": dadd / t_pro / fp64_peak,
                               "hbm_achieved_gbs": pro_bytes / t_pro / 1e9, "hbm_peak_gbs": pk["hbm_gbs"],
                               "hbm_frac": pro_bytes / t_pro / 1e9 / pk["hbm_gbs"],
-                              "algorithmic": f"T*K*{a_k} DADD (exact FWHT) and T*(3K+4)+4K+4G bytes per call"},
+                              "algorithmic": f"T*K*{a_k} DADD (exact FWHT) and T*(3K+4)+4K+4G bytes per call",
+                              "note": "issue-bound, not FP64-bound: 37.8 executed instructions per element of which 12 "
+                                      "DADD, 8 warps/SM at 255 registers (profiles/ncu_r2f1.txt, DESIGN.md 7)"},
         "headline_context": {k: {kk: extras[k].get(kk) for kk in ("tops", "ms_per_step", "rrs_overhead_vs_plain_gemm")}
                              for k in ("c3_llama3_8b_down", "c3_llama3_8b_mlp") if k in extras},
         "e2e": {"value": head["e2e_tops"], "unit": "TOPS", "h2d_bytes_per_step": head["h2d"],

@@ -129,7 +129,11 @@ size_t carve(void* base, int64_t T, int64_t N, int64_t K, int32_t group, int32_t
   ws.Xq8 = static_cast<int8_t*>(take((size_t)T * K));
   ws.y_shard = nullptr;
   ws.y_gather = nullptr;
-  ws.part = (T > 0 && T <= kSplitMaxT) ? static_cast<float*>(take(sizeof(float) * kMaxSplits * (size_t)T * N)) : nullptr;
+  // split-K partials only where choose_splits can pick more than one split: decode-sized T, no communicator, N % 4 == 0
+  // and few enough 240-column tiles that two splits of each fit on the GPU (<= 160 SMs on any sm_100 part); otherwise
+  // (e.g. T = 128, N = 28672) the 8 T N floats would be dead scratch
+  const bool split_ok = T > 0 && T <= kSplitMaxT && world == 0 && N % 4 == 0 && (N + 239) / 240 * 2 <= 160;
+  ws.part = split_ok ? static_cast<float*>(take(sizeof(float) * kMaxSplits * (size_t)T * N)) : nullptr;
   if (world >= 1) {
     const int64_t ns = N / world;
     ws.y_shard = take((size_t)T * ns * 4);

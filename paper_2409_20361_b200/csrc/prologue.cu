@@ -232,9 +232,11 @@ RRS_DEVICE void write_codes(const float (&z)[32], float m, int64_t trow, int K, 
     for (int k = 0; k < 32; k += 4) {
       float q[4];
 #pragma unroll
-      for (int h = 0; h < 4; ++h)  // R10; "+ 0" turns rint's -0 into the canonical +0 (code byte 0x00).  The R11 clamp
-        // never binds here: |z| <= m, so |fl(z fl(7/m))| <= 7 (1 + 2^-24)^2 < 7.5 and rint gives |q| <= 7
-        q[h] = __fadd_rn(rintf(__fmul_rn(z[k + h], r)), 0.0f);
+      for (int h = 0; h < 4; ++h)  // R10 round half to even by the 1.5 * 2^23 magic add (exact: |v| < 2^22, and the sum's
+        // ulp is 1, so RN picks the even neighbour on a tie) -- two FADDs on the FMA pipe instead of FRND, and x - x
+        // gives the canonical +0 for a rounded-to-zero negative (code byte 0x00).  The R11 clamp never binds here:
+        // |z| <= m, so |fl(z fl(7/m))| <= 7 (1 + 2^-24)^2 < 7.5 and the rounding gives |q| <= 7
+        q[h] = __fsub_rn(__fadd_rn(__fmul_rn(z[k + h], r), 12582912.0f), 12582912.0f);
       uint32_t lo, hi;
       asm("{\n\t.reg .b16 t;\n\tcvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\n\tcvt.u32.u16 %0, t;\n\t}"
           : "=r"(lo) : "f"(q[1]), "f"(q[0]));

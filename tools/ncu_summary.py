@@ -36,8 +36,10 @@ def launches(path):
         if len(r) > vi:
             d[r[ki].split("(")[0][:70]].append(float(r[vi].replace(",", "")))
     tot = sum(sum(v) for v in d.values())
+    own = sum(sum(v) for k, v in d.items() if "rrs::" in k) or 1  # the library's kernels only (no flush / copies)
     for k, v in sorted(d.items(), key=lambda kv: -sum(kv[1])):
-        print(f"{k:72s} n={len(v):3d} mean={sum(v)/len(v)/1e3:9.2f} us  share={100*sum(v)/tot:5.1f}%")
+        s_own = f"  share of rrs kernels={100*sum(v)/own:5.1f}%" if "rrs::" in k else ""
+        print(f"{k:72s} n={len(v):3d} mean={sum(v)/len(v)/1e3:9.2f} us  share={100*sum(v)/tot:5.1f}%{s_own}")
 
 
 def report(path):
