@@ -364,8 +364,9 @@ struct GroupSmem {
   static constexpr int STAGE = P::TILE * 2;                             // the bf16 tile (single buffer)
   static constexpr int TBL = P::TILE * 2;                               // 32 u16 offsets per gather chunk
   static constexpr int MAX_TILES = 64;                                  // row tiles a CTA may claim (dynamic rows)
-  static constexpr int BYTES = TILE_D + STAGE + TBL + kMaxG * 4 + 2 * 32 * 4 + 16 + MAX_TILES * 8;
-  // + gmax, red[2][32], barrier, the CTA's tile list
+  static constexpr int BYTES = TILE_D + STAGE + TBL + kMaxG * 4 + 2 * 32 * 4 + 32 + MAX_TILES * 8;
+  // + gmax, red[2][32], barriers (pass-1 stage, unused, pass-2 ring x 2), the CTA's tile list
+  static_assert(2 * P::TILE * 4 <= TILE_D, "pass-2 ring: two f32 tiles over the transpose tile");
   static_assert(P::kPow2 && P::THREADS == P::R * P::TP2 && CH * P::TP2 == TPQ && CH <= 2, "gather chunks");
   // the f32 X~ tile is stored with one pad word per 32 (row stride K + K/32): a reorder that maps a warp's lanes to
   // columns 32 apart (e.g. the identity) would otherwise put all 32 gathers of an instruction in one bank
@@ -390,7 +391,8 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   unsigned* gmax_sm = reinterpret_cast<unsigned*>(smem + S::TILE_D + S::STAGE + S::TBL);
   float* red = reinterpret_cast<float*>(gmax_sm + kMaxG);
   uint64_t* bar = reinterpret_cast<uint64_t*>(red + 2 * 32);
-  int64_t* tiles_sm = reinterpret_cast<int64_t*>(bar + 2);  // [MAX_TILES]: the row tiles this CTA transformed
+  uint64_t* bar2 = bar + 2;                                 // pass-2 ring (two f32 tiles over the transpose tile)
+  int64_t* tiles_sm = reinterpret_cast<int64_t*>(bar + 4);  // [MAX_TILES]: the row tiles this CTA transformed
   unsigned* gmax = g_group_gmax[slot];
   unsigned* gbar = g_group_bar[slot];
   const int tid = threadIdx.x;
@@ -407,6 +409,8 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   };
   if (tid == 0) {
     ptx::mbar_init(bar, 1);
+    ptx::mbar_init(&bar2[0], 1);
+    ptx::mbar_init(&bar2[1], 1);
     ptx::fence_barrier_init();
   }
   __syncthreads();
@@ -516,21 +520,22 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   for (int g = tid; g < G; g += P::THREADS)
     if (gmax_sm[g]) atomicMax(gmax + g, gmax_sm[g]);
 
-  // pass 2 reads back exactly the values this thread stored in pass 1 (same rows, same chunks), so its first row is
-  // loaded before the grid barrier (program order makes the thread's own stores visible to its loads); later rows are
-  // prefetched one row ahead in registers
-  auto load_row = [&](int64_t tile, float4 (&x)[CH][8]) {
-    const int64_t trow = tile * P::R + rr;
-    const bool live = tile < ntiles && trow < T;
-#pragma unroll
-    for (int ch = 0; ch < CH; ++ch) {
-      const float4* src = reinterpret_cast<const float4*>(Xr + (live ? trow : 0) * K) + cp + ch * TP2;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) x[ch][q] = live ? __ldcg(src + q * TPQ) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+  // pass 2 reads back this CTA's own pass-1 rows (the same tiles), so the first two are brought into shared memory
+  // (two f32 tiles over the idle transpose tile) by bulk copies issued BEFORE the grid barrier: their latency hides
+  // behind the barrier wait, and every later tile is fetched two tiles ahead.  Every thread's X~ stores are ordered
+  // before the async-proxy reads by its own proxy fence and the CTA barrier that follows.
+  float* ring = reinterpret_cast<float*>(smem);
+  auto issue2 = [&](int i) {  // tile list entry i -> ring slot i & 1
+    const int64_t tile = tiles_sm[i];
+    const int64_t rows = (T - tile * P::R) < P::R ? (T - tile * P::R) : P::R;
+    const uint32_t bytes = (uint32_t)(rows * K * 4);
+    ptx::mbar_arrive_expect_tx(&bar2[i & 1], bytes);
+    ptx::bulk_load(ring + (i & 1) * P::TILE, Xr + tile * P::R * K, bytes, &bar2[i & 1]);
   };
-  float4 xn[CH][8];
-  load_row(ntl > 0 ? tiles_sm[0] : ntiles, xn);
+  ptx::fence_proxy_async_global();
+  __syncthreads();
+  if (tid == 0)
+    for (int i = 0; i < 2 && i < ntl; ++i) issue2(i);
 
   // ---- grid barrier: the Xr stores and the gmax atomics are visible everywhere
   __threadfence();
@@ -574,19 +579,15 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
     const int64_t tile = tiles_sm[i];
     const int64_t trow = tile * P::R + rr;
     const bool live = trow < T;
-    float4 xc[CH][8];
-#pragma unroll
-    for (int ch = 0; ch < CH; ++ch)
-#pragma unroll
-      for (int q = 0; q < 8; ++q) xc[ch][q] = xn[ch][q];
-    load_row(i + 1 < ntl ? tiles_sm[i + 1] : ntiles, xn);  // the next row's loads fly while this row is quantised
+    ptx::mbar_wait(&bar2[i & 1], (i >> 1) & 1);
+    const float4* src = reinterpret_cast<const float4*>(ring + (i & 1) * P::TILE + rr * K);
     float z[CH][32];
     float m = 0.0f;
 #pragma unroll
     for (int ch = 0; ch < CH; ++ch) {
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
-        const float4 x = xc[ch][q];
+        const float4 x = live ? src[q * TPQ + cp + ch * TP2] : make_float4(0.f, 0.f, 0.f, 0.f);
         z[ch][4 * q] = __fmul_rn(x.x, inv_s[ch]);
         z[ch][4 * q + 1] = __fmul_rn(x.y, inv_s[ch]);
         z[ch][4 * q + 2] = __fmul_rn(x.z, inv_s[ch]);
@@ -595,6 +596,8 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
                            fmaxf(fabsf(z[ch][4 * q + 2]), fabsf(z[ch][4 * q + 3]))));
       }
     }
+    __syncthreads();  // every thread has read ring slot i & 1: refill it with tile i + 2
+    if (tid == 0 && i + 2 < ntl) issue2(i + 2);
     if constexpr (TP2 <= 32) {
       m = seg_max(m, TP2);
     } else {  // the row's TP2 / 32 warps through red[pr] (double-buffered: one barrier per tile)
@@ -629,7 +632,8 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
 //     per row, grid barrier (cooperative launch; barrier counters in library memory, self-cleaning: no memset).
 //     T = 1 needs neither: chan_max = |X~| of the single row.
 //   * a3-a6 as in the prefill path (quant_row) on the shared-memory row.
-// FWHT of one bf16 row xrow[C * 1024] (shared memory) by the C warps of a CTA, each input converted to fp64 once.
+// FWHT of one bf16 row xrow[C * 1024] (shared memory) by the C warps of a CTA, each input widened to fp64 once (scaled
+// by 2^-896 with bit moves, fwht.cuh: `out` receives scaled values, to be rounded by f64_scaled_to_f32).
 // H_K = H_C (x) H_1024 (index i = 1024 a + b); the butterfly stages commute:
 //   phase A: warp c transforms chunk c (b bits): 5 bits in registers, a warp-private transpose (tw, 32 x 33), 5 bits;
 //            lane l of warp c then holds chunk c at positions 32 j + l (j < 32), stored to y1[1024 c + 32 j + l].
@@ -652,9 +656,9 @@ RRS_DEVICE void row_fwht_two_level(const uint16_t* xrow, double* tr, double* y1,
       const uint4 w = src[q ^ rot];
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {  // bf16 -> f32 (bits) -> f64, exact
-        v[q * 8 + 2 * h] = (double)__uint_as_float(ws[h] << 16);
-        v[q * 8 + 2 * h + 1] = (double)__uint_as_float(ws[h] & 0xFFFF0000u);
+      for (int h = 0; h < 4; ++h) {  // bf16 -> f64 scaled by 2^-896 (bit moves, exact: fwht.cuh), undone at `out`
+        v[q * 8 + 2 * h] = bf16_hi_to_f64_scaled(ws[h] << 16);
+        v[q * 8 + 2 * h + 1] = bf16_hi_to_f64_scaled(ws[h] & 0xFFFF0000u);
       }
     }
     butterflies<5>(v);
@@ -786,7 +790,7 @@ prologue_decode_kernel(const uint16_t* __restrict__ X, int T, const int32_t* __r
   __syncthreads();
   trace(2, 1);
   // ---- a1 (X~ rounded once to f32, natural column order, into xs over the idle transposes)
-  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i] = __double2float_rn(d); });
+  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i] = f64_scaled_to_f32(d); });
   __syncthreads();
   trace(2, 2);
   // ---- a2: c_j = max over all T rows
@@ -908,7 +912,7 @@ prologue_decode_group_kernel(const uint16_t* __restrict__ X, const int32_t* __re
   ptx::mbar_wait(bar_x, 0);
   trace(2, 1);
   // ---- a1 (X~ rounded once to f32, natural column order, padded, into xs over the idle transposes)
-  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i + (i >> 5)] = __double2float_rn(d); });
+  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i + (i >> 5)] = f64_scaled_to_f32(d); });
   __syncthreads();
   trace(2, 2);
   // ---- a2 + a4: this row's maximum over each group of reordered positions (32 | group: a thread's chunk is in one group)
