@@ -87,8 +87,10 @@ int rrs_version(void);
 
 /* Workspace bytes needed by rrs_linear / rrs_rotate_smooth_quant for T tokens:
  * X~[T][K] f32 (the rotated activation, written once by the FWHT pass and read by the quantisation
- * pass) + chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xop[T][K] u8 (+ Y shard and gather
- * buffers when world > 1), each 256-byte aligned.  Returns 0 for invalid arguments. */
+ * pass) + chan_max[K] f32 + s_group[G] f32 + x_scale[T] f32 + Xop[T][K] u8 (+ split-K partials
+ * 8 * T * N f32 for decode-sized T <= 128 without a communicator when N % 4 == 0 and N <= 19200, the shapes whose
+ * single-GPU GEMM may split K; + Y shard and gather buffers when world > 1), each 256-byte aligned.  Returns 0 for
+ * invalid arguments. */
 size_t rrs_workspace_bytes(int64_t T, int64_t N, int64_t K, int32_t group, int32_t world);
 /* Workspace for rrs_linear / rrs_allgather_columns WITH a communicator of `world` ranks (world >= 1; a 1-rank
  * communicator still runs the NCCL path): as above plus the Y shard and all-gather buffers, always. */

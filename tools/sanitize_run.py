@@ -35,7 +35,9 @@ def main():
     layer_case(8, 256, 256)                    # C1: fused prologue (K = 256), single-CTA GEMM
     layer_case(300, 1024, 264)                 # rows prologue (K = 1024), pair GEMM, ragged T and N
     layer_case(130, 14336, 256)                # two-kernel prologue (K = 28 * 512)
+    layer_case(70, 4096, 256)                  # fused prologue on the 64-double plan (K = 4096), dynamic rows, ring
     layer_case(5, 8192, 512, decode=True)      # decode prologue + packed-W GEMM
+    layer_case(1, 8192, 512, decode=True)      # decode prologue without a barrier (T = 1)
     layer_case(40, 2048, 512)                  # decode-sized T through the split-K GEMM
     layer_case(260, 2048, 496, swiglu=True)    # fused SwiGLU epilogue
     layer_case(130, 1024, 256, i8=True)        # int8 carrier
