@@ -68,16 +68,35 @@ struct FwhtPlan {
 template <class P>
 RRS_DEVICE constexpr int swz(int i) { return i + (i >> 4) + P::PAD_C1 * (i >> P::PAD_S1) + P::PAD_C2 * (i >> P::PAD_S2); }
 
-// Input widening without F2F (a quarter-rate conversion on sm_100a, 16/clk/SM against 64 DADD/clk/SM:
+// Input widening.  Alternative to F2F (a quarter-rate conversion on sm_100a, 16/clk/SM against 64 DADD/clk/SM:
 // profiles/micro_r2.txt): the f32 bit pattern h of a bf16 value, read as the HIGH word of a double after moving its
 // exponent+fraction down 3 bits (sign kept), is exactly x * 2^-896 -- the f32 and f64 exponent fields then coincide
 // (e11 = e8), and f32 subnormals land on f64 subnormals with the same bits.  Every FWHT intermediate is scaled by the
 // same power of two (exact: the values stay far above 2^-1074 times their f32 quantum, R3 holds unchanged), and the
 // single rounding to f32 at the end first undoes the scale (one exact DMUL by 2^896).  Finite inputs only.
-RRS_DEVICE double bf16_hi_to_f64_scaled(uint32_t h) {  // h: bf16 bits in the high half (low half zero)
+// Default: F2F.  The bit-move widening removes the quarter-rate conversion but costs ~4 issue slots per element
+// (shift, two masks, a zeroed low word) plus the DMUL that undoes the scale, and the fused prologue is issue-bound at
+// 8 warps/SM: measured A/B (bench/micro/prologue_trace vs prologue_trace_f2f, same box) 58.9 / 57.7 us with bit moves
+// against 55.9 / 54.8 us with F2F at C3 up, equal at C2.  -DRRS_FWHT_BITWIDEN=1 selects the bit moves.
+#ifndef RRS_FWHT_BITWIDEN
+#define RRS_FWHT_BITWIDEN 0
+#endif
+// widen_bf16_hi: bf16 bits in the high half of h (low half zero) -> f64 (x itself, or x * 2^-896 with the bit moves);
+// fwht_round_f32: an FWHT output in that representation -> the correctly rounded f32
+RRS_DEVICE double widen_bf16_hi(uint32_t h) {
+#if RRS_FWHT_BITWIDEN
   return __hiloint2double((int)((h & 0x80000000u) | ((h >> 3) & 0x0FFFE000u)), 0);
+#else
+  return (double)__uint_as_float(h);
+#endif
 }
-RRS_DEVICE float f64_scaled_to_f32(double d) { return __double2float_rn(d * 0x1p896); }
+RRS_DEVICE float fwht_round_f32(double d) {
+#if RRS_FWHT_BITWIDEN
+  return __double2float_rn(d * 0x1p896);
+#else
+  return __double2float_rn(d);
+#endif
+}
 
 // radix-2^r butterflies over the groups v[u*2^r + k], u < E >> r (all stages of a pass in registers)
 template <int r, int E>
@@ -146,8 +165,8 @@ RRS_DEVICE void h28_lean(double (&v)[E], Emit&& emit) {
     S += v[2 * i];
     D += v[2 * i + 1];
   }
-  emit(0, f64_scaled_to_f32(v[0] + D));
-  emit(1, f64_scaled_to_f32(v[1] - S));
+  emit(0, fwht_round_f32(v[0] + D));
+  emit(1, fwht_round_f32(v[1] - S));
 #pragma unroll
   for (int j = 1; j < 14; ++j) {
     double rs = 0.0, rd = 0.0;
@@ -158,8 +177,8 @@ RRS_DEVICE void h28_lean(double (&v)[E], Emit&& emit) {
       rd += v[2 * i + 1];
     }
     const double sj = v[2 * j], dj = v[2 * j + 1];
-    emit(2 * j, f64_scaled_to_f32(fma(2.0, rd, (sj + dj) + (v[1] - D))));
-    emit(2 * j + 1, f64_scaled_to_f32(dj - fma(2.0, rs, (sj + v[0]) - S)));
+    emit(2 * j, fwht_round_f32(fma(2.0, rd, (sj + dj) + (v[1] - D))));
+    emit(2 * j + 1, fwht_round_f32(dj - fma(2.0, rs, (sj + v[0]) - S)));
   }
 }
 
@@ -278,7 +297,7 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], 
   const int tp2 = p2act ? t % P::TP2 : 0;
   tp = P::kPow2 ? tp2 : t;
   if (p2act) {
-    // bf16 -> f64 scaled by 2^-896 (bit moves only, exact for every finite value incl. subnormals)
+    // bf16 -> f64 (exact for every finite value incl. subnormals; widen_bf16_hi)
     const uint16_t* row = stage + rr * P::K;
 #pragma unroll
     for (int kh = 0; kh < P::E / 8; ++kh) {
@@ -286,8 +305,8 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], 
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
       for (int h = 0; h < 4; ++h) {
-        v[kh * 8 + 2 * h] = bf16_hi_to_f64_scaled(ws[h] << 16);
-        v[kh * 8 + 2 * h + 1] = bf16_hi_to_f64_scaled(ws[h] & 0xFFFF0000u);
+        v[kh * 8 + 2 * h] = widen_bf16_hi(ws[h] << 16);
+        v[kh * 8 + 2 * h + 1] = widen_bf16_hi(ws[h] & 0xFFFF0000u);
       }
     }
     butterflies<P::B>(v);
@@ -296,7 +315,7 @@ RRS_DEVICE void fwht_tile(const uint16_t* stage, double* sm, double (&v)[P::E], 
   if constexpr (P::kPow2) {
     if (p2act) {
 #pragma unroll
-      for (int j = 0; j < P::SLOTS; ++j) emit(j, f64_scaled_to_f32(v[j]));
+      for (int j = 0; j < P::SLOTS; ++j) emit(j, fwht_round_f32(v[j]));
     }
   }
 }

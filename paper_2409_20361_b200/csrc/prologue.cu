@@ -632,8 +632,8 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
 //     per row, grid barrier (cooperative launch; barrier counters in library memory, self-cleaning: no memset).
 //     T = 1 needs neither: chan_max = |X~| of the single row.
 //   * a3-a6 as in the prefill path (quant_row) on the shared-memory row.
-// FWHT of one bf16 row xrow[C * 1024] (shared memory) by the C warps of a CTA, each input widened to fp64 once (scaled
-// by 2^-896 with bit moves, fwht.cuh: `out` receives scaled values, to be rounded by f64_scaled_to_f32).
+// FWHT of one bf16 row xrow[C * 1024] (shared memory) by the C warps of a CTA, each input widened to fp64 once
+// (fwht.cuh widen_bf16_hi: `out` receives values in that representation, to be rounded by fwht_round_f32).
 // H_K = H_C (x) H_1024 (index i = 1024 a + b); the butterfly stages commute:
 //   phase A: warp c transforms chunk c (b bits): 5 bits in registers, a warp-private transpose (tw, 32 x 33), 5 bits;
 //            lane l of warp c then holds chunk c at positions 32 j + l (j < 32), stored to y1[1024 c + 32 j + l].
@@ -656,9 +656,9 @@ RRS_DEVICE void row_fwht_two_level(const uint16_t* xrow, double* tr, double* y1,
       const uint4 w = src[q ^ rot];
       const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-      for (int h = 0; h < 4; ++h) {  // bf16 -> f64 scaled by 2^-896 (bit moves, exact: fwht.cuh), undone at `out`
-        v[q * 8 + 2 * h] = bf16_hi_to_f64_scaled(ws[h] << 16);
-        v[q * 8 + 2 * h + 1] = bf16_hi_to_f64_scaled(ws[h] & 0xFFFF0000u);
+      for (int h = 0; h < 4; ++h) {  // bf16 -> f64, exact (fwht.cuh widen_bf16_hi; `out` rounds with fwht_round_f32)
+        v[q * 8 + 2 * h] = widen_bf16_hi(ws[h] << 16);
+        v[q * 8 + 2 * h + 1] = widen_bf16_hi(ws[h] & 0xFFFF0000u);
       }
     }
     butterflies<5>(v);
@@ -790,7 +790,7 @@ prologue_decode_kernel(const uint16_t* __restrict__ X, int T, const int32_t* __r
   __syncthreads();
   trace(2, 1);
   // ---- a1 (X~ rounded once to f32, natural column order, into xs over the idle transposes)
-  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i] = f64_scaled_to_f32(d); });
+  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i] = fwht_round_f32(d); });
   __syncthreads();
   trace(2, 2);
   // ---- a2: c_j = max over all T rows
@@ -912,7 +912,7 @@ prologue_decode_group_kernel(const uint16_t* __restrict__ X, const int32_t* __re
   ptx::mbar_wait(bar_x, 0);
   trace(2, 1);
   // ---- a1 (X~ rounded once to f32, natural column order, padded, into xs over the idle transposes)
-  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i + (i >> 5)] = f64_scaled_to_f32(d); });
+  row_fwht_two_level<C>(xrow, tr, y1, [&](int i, double d) { xs[i + (i >> 5)] = fwht_round_f32(d); });
   __syncthreads();
   trace(2, 2);
   // ---- a2 + a4: this row's maximum over each group of reordered positions (32 | group: a thread's chunk is in one group)
