@@ -355,6 +355,15 @@ struct GroupPlan {
   using P = FwhtPlan<K, (K >= RRS_GROUP_B6_MIN_K ? 6 : 5)>;
 };
 
+// CTAs per cluster of the fused prologue: its cluster only aggregates the grid-barrier arrivals (one per cluster), so it
+// is as small as keeps the arrivals few while every SM stays usable -- 8 one-SM-spanning clusters of 64-thread CTAs left
+// 6 SMs idle (568 of 592 co-resident CTAs); a cluster of 4 fits on one SM.  (-DRRS_GROUP_CLUSTER=8: the former size)
+#ifndef RRS_GROUP_CLUSTER
+#define RRS_GROUP_CLUSTER 4
+#endif
+template <int K>
+__host__ __device__ constexpr int group_cluster() { return RRS_GROUP_CLUSTER; }
+
 template <int K>
 struct GroupSmem {
   using P = typename GroupPlan<K>::P;
@@ -375,7 +384,7 @@ struct GroupSmem {
 };
 
 template <int K>
-__global__ void __cluster_dims__(colmax_cluster<K>(), 1, 1)
+__global__ void __cluster_dims__(group_cluster<K>(), 1, 1)
     __launch_bounds__(GroupPlan<K>::P::THREADS, GroupPlan<K>::P::MIN_BLOCKS)
 prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restrict__ Xr,
                       const int32_t* __restrict__ perm, float* __restrict__ s_group_out, uint8_t* __restrict__ Xq,
@@ -543,7 +552,7 @@ prologue_group_kernel(const uint16_t* __restrict__ X, int64_t T, float* __restri
   if (ptx::cluster_ctarank() == 0 && tid == 0) {
     __threadfence();  // (cumulative: orders the whole cluster's stores and atomics before the arrival)
     atomicAdd(&gbar[0], 1u);
-    const unsigned nclusters = gridDim.x / colmax_cluster<K>();
+    const unsigned nclusters = gridDim.x / group_cluster<K>();
     unsigned v;
     for (;;) {
       asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&gbar[0]) : "memory");
@@ -1187,13 +1196,13 @@ static cudaError_t launch_group_k(const uint16_t* X, int64_t T, float* Xr, const
   // every CTA must be resident at once (grid barrier): the grid is at most the co-resident cluster count, and the
   // launch is COOPERATIVE, so the runtime refuses it (instead of letting it hang) when the grid cannot be co-resident;
   // the caller then falls back to the two-kernel prologue
-  const int max_clusters = max_active_clusters(kern, colmax_cluster<K>(), P::THREADS, smem);
+  const int max_clusters = max_active_clusters(kern, group_cluster<K>(), P::THREADS, smem);
   if (max_clusters < 1) return cudaErrorCooperativeLaunchTooLarge;
   const int64_t tiles = (T + P::R - 1) / P::R;
   const int64_t clusters =
-      std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + colmax_cluster<K>() - 1) / colmax_cluster<K>()));
+      std::max<int64_t>(1, std::min<int64_t>(max_clusters, (tiles + group_cluster<K>() - 1) / group_cluster<K>()));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(clusters * colmax_cluster<K>()));
+  cfg.gridDim = dim3((unsigned)(clusters * group_cluster<K>()));
   cfg.blockDim = dim3(P::THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
