@@ -355,11 +355,11 @@ struct GroupPlan {
   using P = FwhtPlan<K, (K >= RRS_GROUP_B6_MIN_K ? 6 : 5)>;
 };
 
-// CTAs per cluster of the fused prologue: its cluster only aggregates the grid-barrier arrivals (one per cluster), so it
-// is as small as keeps the arrivals few while every SM stays usable -- 8 one-SM-spanning clusters of 64-thread CTAs left
-// 6 SMs idle (568 of 592 co-resident CTAs); a cluster of 4 fits on one SM.  (-DRRS_GROUP_CLUSTER=8: the former size)
+// CTAs per cluster of the fused prologue: its cluster only aggregates the grid-barrier arrivals (one per cluster).
+// Clusters of 4 (which fit on one SM) were measured against 8: the same 568 co-resident CTAs and the same time
+// (tools/gpu_r2ap.sh), so the size stays 8.
 #ifndef RRS_GROUP_CLUSTER
-#define RRS_GROUP_CLUSTER 4
+#define RRS_GROUP_CLUSTER 8
 #endif
 template <int K>
 __host__ __device__ constexpr int group_cluster() { return RRS_GROUP_CLUSTER; }

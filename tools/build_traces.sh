@@ -12,4 +12,4 @@ nvcc $F -o $R/bench/micro/prologue_trace $R/bench/micro/prologue_trace.cu $C/api
 wait
 nvcc $F -DRRS_GROUP_B6_MIN_K=1073741824 -o $R/bench/micro/prologue_trace_b5 $R/bench/micro/prologue_trace.cu $C/api.cu $C/gemm.cu $C/decode.cu $L
 nvcc $F -DRRS_FWHT_BITWIDEN=1 -o $R/bench/micro/prologue_trace_bits $R/bench/micro/prologue_trace.cu $C/api.cu $C/gemm.cu $C/decode.cu $L
-nvcc $F -DRRS_GROUP_CLUSTER=8 -o $R/bench/micro/prologue_trace_c8 $R/bench/micro/prologue_trace.cu $C/api.cu $C/gemm.cu $C/decode.cu $L
+nvcc $F -DRRS_GROUP_CLUSTER=4 -o $R/bench/micro/prologue_trace_c4 $R/bench/micro/prologue_trace.cu $C/api.cu $C/gemm.cu $C/decode.cu $L
