@@ -441,8 +441,8 @@ def run_gpu(args):
                               "hbm_achieved_gbs": pro_bytes / t_pro / 1e9, "hbm_peak_gbs": pk["hbm_gbs"],
                               "hbm_frac": pro_bytes / t_pro / 1e9 / pk["hbm_gbs"],
                               "algorithmic": f"T*K*{a_k} DADD (exact FWHT) and T*(3K+4)+4K+4G bytes per call",
-                              "note": "issue-bound, not FP64-bound: 37.8 executed instructions per element of which 12 "
-                                      "DADD, 8 warps/SM at 255 registers (profiles/ncu_r2f1.txt, DESIGN.md 7)"},
+                              "note": "issue-bound, not FP64-bound: 34 executed instructions per element of which 12 "
+                                      "DADD, 8 warps/SM at 255 registers (profiles/ncu_r2f3.txt, DESIGN.md 7)"},
         "headline_context": {k: {kk: extras[k].get(kk) for kk in ("tops", "ms_per_step", "rrs_overhead_vs_plain_gemm")}
                              for k in ("c3_llama3_8b_down", "c3_llama3_8b_mlp") if k in extras},
         "e2e": {"value": head["e2e_tops"], "unit": "TOPS", "h2d_bytes_per_step": head["h2d"],
