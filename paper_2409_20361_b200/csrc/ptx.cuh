@@ -77,20 +77,6 @@ RRS_DEV float4 ld_dsmem_f32x4(const void* p, uint32_t rank) {
                : "r"(remote));
   return v;
 }
-// 32-bit store into the shared memory of CTA `rank` of this cluster at the address of local `p` (weak; made
-// visible to that CTA by a following cluster barrier)
-RRS_DEV void st_dsmem_f32(void* p, uint32_t rank, float v) {
-  uint32_t remote;
-  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(remote), "f"(v) : "memory");
-}
-// 16-byte store into the shared memory of CTA `rank` (address of local `p`, 16-byte aligned)
-RRS_DEV void st_dsmem_v4(void* p, uint32_t rank, float a, float b, float c, float d) {
-  uint32_t remote;
-  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
-  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(remote), "f"(a), "f"(b), "f"(c), "f"(d)
-               : "memory");
-}
 // the two halves of cluster_sync (arrive with release / wait with acquire), for warps that do work in between
 RRS_DEV void cluster_sync_warps_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 RRS_DEV void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
@@ -110,18 +96,6 @@ RRS_DEV void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
-// wait with cluster-scope acquire: pairs with mbarrier.arrive.release.cluster from a peer CTA
-RRS_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1, %2;\n\t"
-      "@P1 bra DONE_%=;\n\t"
-      "bra WAIT_%=;\n\t"
-      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(0x989680u)
-      : "memory");
-}
 
 // ------------------------------------------------------------------ TMA
 RRS_DEV void prefetch_tmap(const void* tmap) {
@@ -163,16 +137,6 @@ RRS_DEV void tma_load_2d_pair(void* smem_dst, const void* tmap, uint32_t bar_clu
       "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
       " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(bar_cluster_addr), "l"(cache_hint)
-      : "memory");
-}
-// 1-D bulk copy global -> the same shared offset in every CTA of cta_mask (cluster multicast); each
-// destination CTA's mbarrier (same offset) receives the complete_tx of its copy.
-RRS_DEV void bulk_load_multicast(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar,
-                                 uint16_t cta_mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(reinterpret_cast<uint64_t>(gmem_src)), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
       : "memory");
 }
 // 2-D tiled store shared -> global (TMA; out-of-bounds box elements are not written), bulk-group tracked
@@ -221,10 +185,6 @@ RRS_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
 // (no cluster-wide memory fence: enough when the arrive only has to order tcgen05.ld completions)
 RRS_DEV void mbar_arrive_remote(uint32_t bar_cluster_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
-}
-// same with release at cluster scope (orders this thread's prior tcgen05.st for a peer CTA's MMA)
-RRS_DEV void mbar_arrive_cluster(uint32_t bar_cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }
 RRS_DEV void tmem_alloc2(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
@@ -321,15 +281,7 @@ RRS_DEV void mma_commit(uint64_t* bar) {
                :                                                                                         \
                : "memory")
 
-#define RRS_TMEM_ST16_SPLAT(taddr, v)                                                                    \
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" \
-               ::"r"(taddr), "r"(v) : "memory")
 
-// 32 lanes x 8 columns of 32-bit from 8 registers (v[j] -> column j of the thread's lane)
-#define RRS_TMEM_ST8(taddr, v)                                                                           \
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),        \
-               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])        \
-               : "memory")
 
 // 32 lanes x 32 columns of 32-bit from 32 registers (v[j] -> column j of the thread's lane)
 #define RRS_TMEM_ST32(taddr, v)                                                                          \
